@@ -1,0 +1,140 @@
+/*
+ * rutv_b200.h -- C ABI of the B200-native blocked randUTV (librutv_b200.so).
+ *
+ * Drop-in boundary for the reference's hot path
+ *   randutv::UTVResult randutv::randutv(ConstMatrixView a, const UTVConfig& cfg)
+ *   (/root/reference/proj/include/randutv/randutv_blocked.hpp:39,
+ *    implementation proj/src/randutv_blocked.cpp:84-157)
+ * and of the L1 kernels it is built from.  Plain pointers and sizes only; all
+ * matrices are column-major FP64, element (i, j) at p[i + j*ld]
+ * (proj/include/randutv/matrix.hpp:16-28).  No torch types cross this line.
+ *
+ * Every entry point returns an int status (rutv_code) and, when `st` is
+ * non-NULL, fills it with the code, the Jacobi residual for
+ * RUTV_ERR_CONVERGENCE, and a message.  The codes map one-to-one onto the
+ * reference's exception classes (proj/include/randutv/errors.hpp:9-50):
+ * ConfigError -> RUTV_ERR_CONFIG, ShapeError -> RUTV_ERR_SHAPE,
+ * IndexError -> RUTV_ERR_INDEX, ConvergenceError{residual} -> RUTV_ERR_CONVERGENCE.
+ * The C++ shim (include/randutv_b200/randutv.hpp) rethrows those types.
+ */
+#ifndef RUTV_B200_H
+#define RUTV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RUTV_OK = 0,
+    RUTV_ERR_CONFIG = 1,      /* b < 1, q < 0            (randutv_blocked.cpp:10-14) */
+    RUTV_ERR_SHAPE = 2,       /* operand shape mismatch  (gemm.cpp:11-17)            */
+    RUTV_ERR_INDEX = 3,       /* view out of range       (matrix.hpp:30-36)          */
+    RUTV_ERR_CONVERGENCE = 4, /* Jacobi sweep cap hit    (jacobi_svd.cpp:97-109)     */
+    RUTV_ERR_CUDA = 5,
+    RUTV_ERR_NCCL = 6,
+    RUTV_ERR_OOM = 7,
+    RUTV_ERR_NOTIMPL = 8,
+    RUTV_ERR_INTERNAL = 9
+} rutv_code;
+
+typedef struct {
+    int32_t code;
+    int32_t reserved;
+    double residual; /* ConvergenceError::residual (errors.hpp:29-33) */
+    char message[256];
+} rutv_status;
+
+/* Mirror of randutv::UTVConfig (randutv_blocked.hpp:11-20) plus device-side knobs. */
+typedef struct {
+    int64_t b;          /* block size, >= 1 (reference default 128)          */
+    int32_t q;          /* power iterations, >= 0 (reference default 1)      */
+    int32_t build_u;    /* 0: U is not formed (reference returns 0x0 U)      */
+    int32_t build_v;
+    int32_t qr_prepass; /* reference qr_prepass (m > n only)                 */
+    uint64_t seed;      /* Gaussian sketch stream seed (RngState, rng.hpp:18) */
+    int32_t device;     /* CUDA device ordinal                               */
+    int32_t max_steps;  /* < 0: run to completion; else stop after k steps   */
+    int32_t overlap;    /* 1: off-critical-path updates on a second stream  */
+    int32_t reserved[7];
+} rutv_opts;
+
+/* Fills the reference defaults: b=128, q=1, build_u=build_v=1, seed=0,
+ * device=0, max_steps=-1, overlap=1. */
+void rutv_b200_default_opts(rutv_opts* o);
+
+/* Number of Gaussian deviates the blocked driver draws for an m x n input:
+ * sum over full steps of rows_rem*b (randutv_blocked.cpp:41-44, 122-139). */
+int64_t rutv_b200_stream_length(int64_t m, int64_t n, int64_t b);
+
+/* Algorithmic flop count F(n, b, q) of SURVEY.md section 8(a) (U and V built). */
+double rutv_b200_flops(int64_t n, int64_t b, int32_t q);
+
+/*
+ * randutv::randutv replacement.  HOST pointers.
+ *   A (m x n, lda) is read only.
+ *   G: NULL -> the sketch is drawn on the device from RngState(o->seed)
+ *      (counter-based, same stream positions as the reference; libm-level
+ *      ulp differences possible in log/sin/cos);
+ *      non-NULL -> the first g_len deviates of the reference stream, i.e.
+ *      G[d] = RngState(seed).normal_at(d); g_len must be >=
+ *      rutv_b200_stream_length(m, n, b).  This is the bit-identical parity mode.
+ *   T (m x n, ldt), U (m x m, ldu), V (n x n, ldv) are written; U / V may be
+ *   NULL when build_u / build_v is 0.
+ */
+int rutv_b200_factorize(const rutv_opts* o, const double* A, int64_t m, int64_t n, int64_t lda,
+                        const double* G, int64_t g_len, double* T, int64_t ldt, double* U,
+                        int64_t ldu, double* V, int64_t ldv, rutv_status* st);
+
+/* Same, DEVICE pointers (no host copies; for resident-input benchmarking).
+ * A is read only; T/U/V are device buffers on o->device. */
+int rutv_b200_factorize_device(const rutv_opts* o, const double* dA, int64_t m, int64_t n,
+                               int64_t lda, const double* dG, int64_t g_len, double* dT,
+                               int64_t ldt, double* dU, int64_t ldu, double* dV, int64_t ldv,
+                               rutv_status* st);
+
+/* Per-phase device timings (ms) of the last factorize call on this thread
+ * when RUTV_PROFILE=1; returns the number of phases written (<= cap). */
+int rutv_b200_last_profile(const char** names, double* ms, int cap);
+
+/* Kernels this library launched since load (evidence for bench.py). */
+uint64_t rutv_b200_launch_count(void);
+
+/* ---------------- L1 kernels (DEVICE pointers, stream 0 of o->device) ---------------- */
+
+/* gemm (proj/src/gemm.cpp:21, contract matrix_ops.hpp:9-18):
+ * C <- alpha op(A) op(B) + beta C; ta/tb: 0 = N, 1 = T. */
+int rutv_b200_gemm(int device, double alpha, int ta, const double* A, int64_t ar, int64_t ac,
+                   int64_t lda, int tb, const double* B, int64_t br, int64_t bc, int64_t ldb,
+                   double beta, double* C, int64_t m, int64_t n, int64_t ldc, rutv_status* st);
+
+/* hqr_inplace + form_wy_t (householder.cpp:48-97): packed QR of A (m x n) in
+ * place, tau[min(m,n)], Twy (p x p, ldt) with p = min(m, n). */
+int rutv_b200_hqr(int device, double* A, int64_t m, int64_t n, int64_t lda, double* tau,
+                  double* twy, int64_t ldt, rutv_status* st);
+
+/* apply_q_right (householder.cpp:129-140): B (rows x s) <- B Q, Q = I - W Twy W'. */
+int rutv_b200_apply_q_right(int device, const double* qr, int64_t s, int64_t ldq,
+                            const double* twy, int64_t p, int64_t ldt, double* B, int64_t rows,
+                            int64_t ldb, rutv_status* st);
+/* apply_qt_left (householder.cpp:103-114): B (s x cols) <- Q' B. */
+int rutv_b200_apply_qt_left(int device, const double* qr, int64_t s, int64_t ldq,
+                            const double* twy, int64_t p, int64_t ldt, double* B, int64_t cols,
+                            int64_t ldb, rutv_status* st);
+
+/* svd_block (jacobi_svd.cpp:39-148): one-sided Jacobi SVD of a square block.
+ * U, V n x n (ld n), sigma[n] descending. */
+int rutv_b200_svd_block(int device, const double* A, int64_t n, int64_t lda, double tol,
+                        int max_sweeps, double* U, double* sigma, double* V, rutv_status* st);
+
+/* generate_normal_random (rng.cpp:44-53): G (rows x cols, ldg) from stream
+ * position pos, column-major. */
+int rutv_b200_normal_fill(int device, uint64_t seed, uint64_t pos, double* G, int64_t rows,
+                          int64_t cols, int64_t ldg, rutv_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RUTV_B200_H */

@@ -1,0 +1,267 @@
+"""B200-native blocked randUTV (A = U T V^T) -- Python mirror of the reference API.
+
+The reference exposes ``randutv.factorize(a, *, b=0, q=1, algo="blocked",
+workers=1, seed=0, build_uv=True, qr_prepass=False) -> (t, u, v)``
+(/root/reference/proj/python/bindings.cpp:49-66, 123-132).  ``factorize`` here
+keeps that signature and return convention and adds ``algo="b200"`` (the
+default) plus ``g=`` for an explicit Gaussian stream.  It calls the C ABI in
+``librutv_b200.so`` (include/rutv_b200.h) -- hand-written sm_100a kernels, no
+cuBLAS/cuSOLVER and no CPU fallback: if the library or a GPU is missing the
+call raises.
+
+Exception mapping follows bindings.cpp:109-121: ConfigError / ShapeError ->
+ValueError, IndexError -> IndexError, ConvergenceError -> ConvergenceError
+(a RuntimeError carrying ``.residual``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librutv_b200.so")
+
+__all__ = ["factorize", "factorize_device", "flops", "stream_length", "ConvergenceError",
+           "RutvError", "lib", "gemm", "hqr", "svd_block", "normal_fill", "apply_q_right",
+           "apply_qt_left", "launch_count", "last_profile"]
+
+RUTV_OK, RUTV_ERR_CONFIG, RUTV_ERR_SHAPE, RUTV_ERR_INDEX, RUTV_ERR_CONVERGENCE = 0, 1, 2, 3, 4
+RUTV_ERR_CUDA, RUTV_ERR_NCCL, RUTV_ERR_OOM, RUTV_ERR_NOTIMPL, RUTV_ERR_INTERNAL = 5, 6, 7, 8, 9
+
+
+class RutvError(RuntimeError):
+    def __init__(self, code: int, message: str, residual: float = 0.0):
+        super().__init__(message)
+        self.code = code
+        self.residual = residual
+
+
+class ConvergenceError(RutvError):
+    """Jacobi sweep cap hit (reference ConvergenceError, errors.hpp:29-33)."""
+
+
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("reserved", C.c_int32), ("residual", C.c_double),
+                ("message", C.c_char * 256)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("b", C.c_int64), ("q", C.c_int32), ("build_u", C.c_int32), ("build_v", C.c_int32),
+                ("qr_prepass", C.c_int32), ("seed", C.c_uint64), ("device", C.c_int32),
+                ("max_steps", C.c_int32), ("overlap", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+_D = C.POINTER(C.c_double)
+_I64 = C.c_int64
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load librutv_b200.so (building it in place if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    from . import _build
+    if not _build.up_to_date():
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: the B200 path has no fallback")
+    L = C.CDLL(LIB_PATH)
+    L.rutv_b200_default_opts.argtypes = [C.POINTER(Opts)]
+    L.rutv_b200_stream_length.argtypes = [_I64, _I64, _I64]
+    L.rutv_b200_stream_length.restype = _I64
+    L.rutv_b200_flops.argtypes = [_I64, _I64, C.c_int32]
+    L.rutv_b200_flops.restype = C.c_double
+    fac = [C.POINTER(Opts), C.c_void_p, _I64, _I64, _I64, C.c_void_p, _I64, C.c_void_p, _I64,
+           C.c_void_p, _I64, C.c_void_p, _I64, C.POINTER(Status)]
+    L.rutv_b200_factorize.argtypes = fac
+    L.rutv_b200_factorize_device.argtypes = fac
+    L.rutv_b200_last_profile.argtypes = [C.POINTER(C.c_char_p), _D, C.c_int]
+    L.rutv_b200_launch_count.restype = C.c_uint64
+    L.rutv_b200_gemm.argtypes = [C.c_int, C.c_double, C.c_int, C.c_void_p, _I64, _I64, _I64, C.c_int,
+                                 C.c_void_p, _I64, _I64, _I64, C.c_double, C.c_void_p, _I64, _I64,
+                                 _I64, C.POINTER(Status)]
+    L.rutv_b200_hqr.argtypes = [C.c_int, C.c_void_p, _I64, _I64, _I64, C.c_void_p, C.c_void_p, _I64,
+                                C.POINTER(Status)]
+    L.rutv_b200_apply_q_right.argtypes = [C.c_int, C.c_void_p, _I64, _I64, C.c_void_p, _I64, _I64,
+                                          C.c_void_p, _I64, _I64, C.POINTER(Status)]
+    L.rutv_b200_apply_qt_left.argtypes = L.rutv_b200_apply_q_right.argtypes
+    L.rutv_b200_svd_block.argtypes = [C.c_int, C.c_void_p, _I64, _I64, C.c_double, C.c_int,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Status)]
+    L.rutv_b200_normal_fill.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, _I64, _I64,
+                                        _I64, C.POINTER(Status)]
+    _lib = L
+    return L
+
+
+def _raise(st: Status) -> None:
+    if st.code == RUTV_OK:
+        return
+    msg = st.message.decode(errors="replace")
+    if st.code in (RUTV_ERR_CONFIG, RUTV_ERR_SHAPE):
+        raise ValueError(msg)
+    if st.code == RUTV_ERR_INDEX:
+        raise IndexError(msg)
+    if st.code == RUTV_ERR_CONVERGENCE:
+        raise ConvergenceError(st.code, msg, st.residual)
+    raise RutvError(st.code, msg, st.residual)
+
+
+def make_opts(b: int = 128, q: int = 1, seed: int = 0, build_u: bool = True, build_v: bool = True,
+              qr_prepass: bool = False, device: int = 0, max_steps: int = -1,
+              overlap: bool = True) -> Opts:
+    o = Opts()
+    lib().rutv_b200_default_opts(C.byref(o))
+    o.b, o.q, o.seed = int(b), int(q), int(seed)
+    o.build_u, o.build_v, o.qr_prepass = int(build_u), int(build_v), int(qr_prepass)
+    o.device, o.max_steps, o.overlap = int(device), int(max_steps), int(overlap)
+    return o
+
+
+def stream_length(m: int, n: int, b: int) -> int:
+    """Gaussian deviates the blocked driver draws (randutv_blocked.cpp:41-44)."""
+    return int(lib().rutv_b200_stream_length(m, n, b))
+
+
+def flops(n: int, b: int, q: int) -> float:
+    """Algorithmic flop count F(n, b, q) (U and V built)."""
+    return float(lib().rutv_b200_flops(n, b, q))
+
+
+def _ptr(x: np.ndarray):
+    return x.ctypes.data_as(C.c_void_p)
+
+
+def factorize(a, *, b: int = 0, q: int = 1, algo: str = "b200", seed: int = 0,
+              build_uv: bool = True, qr_prepass: bool = False, g=None, device: int = 0,
+              max_steps: int = -1):
+    """Factor ``a`` as ``u @ t @ v.T`` on the B200 (bindings.cpp:49-66 semantics).
+
+    ``g``: optional 1-D array with the first ``stream_length(m, n, b)`` deviates
+    of ``RngState(seed)`` -- the bit-identical parity mode; otherwise the sketch
+    is drawn on the device from the same counter-based stream.
+    Returns ``(t, u, v)``; ``u``/``v`` are None when ``build_uv`` is False."""
+    if algo != "b200":
+        raise ValueError(f"algo must be 'b200' on this build, got '{algo}'")
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2:
+        raise ValueError("expected a 2-d array")
+    m, n = a.shape
+    bb = b if b > 0 else 128
+    o = make_opts(b=bb, q=q, seed=seed, build_u=build_uv, build_v=build_uv,
+                  qr_prepass=qr_prepass, device=device, max_steps=max_steps)
+    t = np.zeros((m, n), order="F")
+    u = np.zeros((m, m), order="F") if build_uv else None
+    v = np.zeros((n, n), order="F") if build_uv else None
+    gp, glen = None, 0
+    if g is not None:
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        gp, glen = _ptr(g), g.size
+    st = Status()
+    lib().rutv_b200_factorize(C.byref(o), _ptr(a), m, n, max(m, 1), gp, glen, _ptr(t), max(m, 1),
+                              _ptr(u) if u is not None else None, max(m, 1),
+                              _ptr(v) if v is not None else None, max(n, 1), C.byref(st))
+    _raise(st)
+    return t, u, v
+
+
+def factorize_device(a, t, u=None, v=None, *, b: int = 128, q: int = 1, seed: int = 0,
+                     g=None, device: int | None = None, max_steps: int = -1) -> None:
+    """Device-resident variant on torch CUDA tensors (column-major = a
+    transposed contiguous row-major tensor; pass ``x.T`` views with stride (1, ld))."""
+    def info(x):
+        if x is None:
+            return None, 1
+        assert x.dtype.itemsize == 8 and x.stride(0) == 1, "column-major fp64 tensor expected"
+        return C.c_void_p(x.data_ptr()), max(x.stride(1), x.shape[0], 1)
+    m, n = a.shape
+    dev = a.device.index if device is None else device
+    o = make_opts(b=b, q=q, seed=seed, build_u=u is not None, build_v=v is not None, device=dev,
+                  max_steps=max_steps)
+    pa, lda = info(a)
+    pt, ldt = info(t)
+    pu, ldu = info(u)
+    pv, ldv = info(v)
+    gp, glen = (C.c_void_p(g.data_ptr()), g.numel()) if g is not None else (None, 0)
+    st = Status()
+    lib().rutv_b200_factorize_device(C.byref(o), pa, m, n, lda, gp, glen, pt, ldt, pu, ldu, pv, ldv,
+                                     C.byref(st))
+    _raise(st)
+
+
+def launch_count() -> int:
+    return int(lib().rutv_b200_launch_count())
+
+
+def last_profile() -> dict:
+    names = (C.c_char_p * 16)()
+    ms = (C.c_double * 16)()
+    k = lib().rutv_b200_last_profile(names, ms, 16)
+    return {names[i].decode(): ms[i] for i in range(k)}
+
+
+# ---------------- L1 kernels on torch CUDA tensors (column-major views) ----------------
+
+def _cm(x):
+    """(ptr, rows, cols, ld) of a column-major fp64 CUDA tensor view (stride(0) == 1)."""
+    assert x.is_cuda and x.stride(0) == 1 or x.numel() == 0, "column-major CUDA tensor expected"
+    r, c = x.shape
+    return C.c_void_p(x.data_ptr()), r, c, max(x.stride(1) if c > 1 else r, r, 1)
+
+
+def gemm(alpha, ta, a, tb, b, beta, c) -> None:
+    """In-place ``c <- alpha op(a) op(b) + beta c`` (proj/src/gemm.cpp:21)."""
+    pa, ar, ac, lda = _cm(a)
+    pb, br, bc, ldb = _cm(b)
+    pc, m, n, ldc = _cm(c)
+    st = Status()
+    lib().rutv_b200_gemm(c.device.index, alpha, int(ta), pa, ar, ac, lda, int(tb), pb, br, bc, ldb,
+                         beta, pc, m, n, ldc, C.byref(st))
+    _raise(st)
+
+
+def hqr(a, tau, twy) -> None:
+    """In-place packed QR + Twy (householder.cpp:48-97)."""
+    pa, m, n, lda = _cm(a)
+    pt, p, _, ldt = _cm(twy)
+    st = Status()
+    lib().rutv_b200_hqr(a.device.index, pa, m, n, lda, C.c_void_p(tau.data_ptr()), pt, ldt,
+                        C.byref(st))
+    _raise(st)
+
+
+def apply_q_right(qr, twy, bmat) -> None:
+    pq, s, p, ldq = _cm(qr)
+    pt, _, _, ldt = _cm(twy)
+    pb, rows, _, ldb = _cm(bmat)
+    st = Status()
+    lib().rutv_b200_apply_q_right(bmat.device.index, pq, s, ldq, pt, twy.shape[0], ldt, pb, rows, ldb,
+                                  C.byref(st))
+    _raise(st)
+
+
+def apply_qt_left(qr, twy, bmat) -> None:
+    pq, s, p, ldq = _cm(qr)
+    pt, _, _, ldt = _cm(twy)
+    pb, _, cols, ldb = _cm(bmat)
+    st = Status()
+    lib().rutv_b200_apply_qt_left(bmat.device.index, pq, s, ldq, pt, twy.shape[0], ldt, pb, cols,
+                                  ldb, C.byref(st))
+    _raise(st)
+
+
+def svd_block(a, u, sigma, v, tol: float = 1e-15, max_sweeps: int = 30) -> None:
+    pa, n, _, lda = _cm(a)
+    st = Status()
+    lib().rutv_b200_svd_block(a.device.index, pa, n, lda, tol, max_sweeps, C.c_void_p(u.data_ptr()),
+                              C.c_void_p(sigma.data_ptr()), C.c_void_p(v.data_ptr()), C.byref(st))
+    _raise(st)
+
+
+def normal_fill(seed: int, pos: int, g) -> None:
+    pg, r, c, ld = _cm(g)
+    st = Status()
+    lib().rutv_b200_normal_fill(g.device.index, seed, pos, pg, r, c, ld, C.byref(st))
+    _raise(st)

@@ -1,0 +1,389 @@
+// gemm_f64.cu -- FP64 tensor-core GEMM for sm_100a (warp-level DMMA).
+//
+// Replaces the reference's single scalar gemm (proj/src/gemm.cpp:21-75,
+// contract proj/include/randutv/matrix_ops.hpp:9-18), which carries 95% of
+// the reference's wall time.  On sm_100a the only FP64
+// tensor path is the legacy warp-level mma.sync .f64 (ptxas rejects
+// tcgen05.mma kind::f64); every PTX shape lowers to SASS DMMA.8x8x4 and all
+// reach the same measured peak (profiles/r01_dmma_peak.jsonl: 37.1 TF/s), so
+// the kernel issues m16n8k4 and spends its effort on feeding it:
+//   * cp.async multistage shared-memory pipeline (3 stages), 16-byte chunks
+//     when operands are 16-byte aligned, 8-byte otherwise (odd b / ld);
+//   * smem tiles stored in the operand's contiguous global direction with a
+//     +4-double pad so every fragment load is bank-conflict free for all four
+//     transpose combinations;
+//   * two CTA tiles: 128x128 (8 warps, 64x32 warp tiles) for the large
+//     rank-b updates, 64x64 (4 warps) + deterministic split-K for the
+//     tall-skinny K = s sketch / projection products;
+//   * split-K partials are summed in a fixed order by a separate kernel, so
+//     results are bit-reproducible run to run.
+#include <algorithm>
+#include <atomic>
+
+#include "rutv_common.cuh"
+
+namespace rutv {
+
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launch_count() { return g_launches.load(); }
+void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+struct GemmParams {
+    int64_t M, N, K;
+    const double* A;
+    int64_t lda;
+    const double* B;
+    int64_t ldb;
+    double* C;
+    int64_t ldc;
+    double alpha, beta;
+    double* work;
+    int64_t kchunk;
+    int splits;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma_16x8x4(double* c, const double* a, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};\n"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a[0]), "d"(a[1]), "d"(b));
+}
+
+template <int BM, int BN, int BK, bool TA, bool TB>
+struct SmemGeom {
+    static constexpr int A_LD = TA ? (BK + 4) : (BM + 4);
+    static constexpr int A_SZ = TA ? BM * A_LD : BK * A_LD;
+    static constexpr int B_LD = TB ? (BN + 4) : (BK + 4);
+    static constexpr int B_SZ = TB ? BK * B_LD : BN * B_LD;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, bool VEC>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    dgemm_kernel(const GemmParams p) {
+    constexpr int NWM = BM / WM, NWN = BN / WN, NT = NWM * NWN * 32;
+    constexpr int MI = WM / 16, NI = WN / 8;
+    using G = SmemGeom<BM, BN, BK, TA, TB>;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + ST * G::A_SZ;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % NWM, wn = warp / NWM;
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BN;
+    const int64_t kbeg = static_cast<int64_t>(blockIdx.z) * p.kchunk;
+    const int64_t kend = min(p.K, kbeg + p.kchunk);
+    const int KT = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
+    const int64_t M = p.M, N = p.N;
+
+    auto load_tile = [&](int stage, int64_t k0) {
+        double* as = As + stage * G::A_SZ;
+        double* bs = Bs + stage * G::B_SZ;
+        if constexpr (!TA) {  // op(A)(m,k) = A[m + k*lda]; smem as[k][m]
+            if constexpr (VEC) {
+                for (int c = tid; c < BK * BM / 2; c += NT) {
+                    const int k = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+                    const int64_t gm = m0 + mm, gk = k0 + k;
+                    int bytes = 0;
+                    const double* src = p.A;
+                    if (gk < kend && gm < M) {
+                        bytes = gm + 1 < M ? 16 : 8;
+                        src = p.A + gm + gk * p.lda;
+                    }
+                    cp_async16(as + k * G::A_LD + mm, src, bytes);
+                }
+            } else {
+                for (int c = tid; c < BK * BM; c += NT) {
+                    const int k = c / BM, mm = c % BM;
+                    const int64_t gm = m0 + mm, gk = k0 + k;
+                    const bool ok = gk < kend && gm < M;
+                    cp_async8(as + k * G::A_LD + mm, ok ? p.A + gm + gk * p.lda : p.A, ok ? 8 : 0);
+                }
+            }
+        } else {  // op(A)(m,k) = A[k + m*lda]; smem as[m][k]
+            if constexpr (VEC) {
+                for (int c = tid; c < BM * BK / 2; c += NT) {
+                    const int mm = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+                    const int64_t gm = m0 + mm, gk = k0 + kk;
+                    int bytes = 0;
+                    const double* src = p.A;
+                    if (gk < kend && gm < M) {
+                        bytes = gk + 1 < kend ? 16 : 8;
+                        src = p.A + gk + gm * p.lda;
+                    }
+                    cp_async16(as + mm * G::A_LD + kk, src, bytes);
+                }
+            } else {
+                for (int c = tid; c < BM * BK; c += NT) {
+                    const int mm = c / BK, kk = c % BK;
+                    const int64_t gm = m0 + mm, gk = k0 + kk;
+                    const bool ok = gk < kend && gm < M;
+                    cp_async8(as + mm * G::A_LD + kk, ok ? p.A + gk + gm * p.lda : p.A, ok ? 8 : 0);
+                }
+            }
+        }
+        if constexpr (!TB) {  // op(B)(k,n) = B[k + n*ldb]; smem bs[n][k]
+            if constexpr (VEC) {
+                for (int c = tid; c < BN * BK / 2; c += NT) {
+                    const int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+                    const int64_t gn = n0 + nn, gk = k0 + kk;
+                    int bytes = 0;
+                    const double* src = p.B;
+                    if (gk < kend && gn < N) {
+                        bytes = gk + 1 < kend ? 16 : 8;
+                        src = p.B + gk + gn * p.ldb;
+                    }
+                    cp_async16(bs + nn * G::B_LD + kk, src, bytes);
+                }
+            } else {
+                for (int c = tid; c < BN * BK; c += NT) {
+                    const int nn = c / BK, kk = c % BK;
+                    const int64_t gn = n0 + nn, gk = k0 + kk;
+                    const bool ok = gk < kend && gn < N;
+                    cp_async8(bs + nn * G::B_LD + kk, ok ? p.B + gk + gn * p.ldb : p.B, ok ? 8 : 0);
+                }
+            }
+        } else {  // op(B)(k,n) = B[n + k*ldb]; smem bs[k][n]
+            if constexpr (VEC) {
+                for (int c = tid; c < BK * BN / 2; c += NT) {
+                    const int k = c / (BN / 2), nn = (c % (BN / 2)) * 2;
+                    const int64_t gn = n0 + nn, gk = k0 + k;
+                    int bytes = 0;
+                    const double* src = p.B;
+                    if (gk < kend && gn < N) {
+                        bytes = gn + 1 < N ? 16 : 8;
+                        src = p.B + gn + gk * p.ldb;
+                    }
+                    cp_async16(bs + k * G::B_LD + nn, src, bytes);
+                }
+            } else {
+                for (int c = tid; c < BK * BN; c += NT) {
+                    const int k = c / BN, nn = c % BN;
+                    const int64_t gn = n0 + nn, gk = k0 + k;
+                    const bool ok = gk < kend && gn < N;
+                    cp_async8(bs + k * G::B_LD + nn, ok ? p.B + gn + gk * p.ldb : p.B, ok ? 8 : 0);
+                }
+            }
+        }
+    };
+
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < KT) load_tile(s, kbeg + static_cast<int64_t>(s) * BK);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        const int nk = kt + ST - 1;
+        if (nk < KT) load_tile(nk % ST, kbeg + static_cast<int64_t>(nk) * BK);
+        cp_async_commit();
+        const double* as = As + (kt % ST) * G::A_SZ;
+        const double* bs = Bs + (kt % ST) * G::B_SZ;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[MI][2], bf[NI];
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int mr = wm * WM + mi * 16 + g + 8 * h, kc = kk + t;
+                    af[mi][h] = TA ? as[mr * G::A_LD + kc] : as[kc * G::A_LD + mr];
+                }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const int nc = wn * WN + ni * 8 + g, kr = kk + t;
+                bf[ni] = TB ? bs[kr * G::B_LD + nc] : bs[nc * G::B_LD + kr];
+            }
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) dmma_16x8x4(acc[mi][ni], af[mi], bf[ni]);
+        }
+    }
+    cp_async_wait<0>();
+
+    const bool direct = p.splits == 1;
+    double* wbase = p.work + static_cast<int64_t>(blockIdx.z) * M * N;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t m = m0 + wm * WM + mi * 16 + g + (r >= 2 ? 8 : 0);
+                const int64_t n = n0 + wn * WN + ni * 8 + 2 * t + (r & 1);
+                if (m < M && n < N) {
+                    if (direct) {
+                        double* cp = p.C + m + n * p.ldc;
+                        double v = p.alpha * acc[mi][ni][r];
+                        if (p.beta != 0.0) v += p.beta * *cp;
+                        *cp = v;
+                    } else {
+                        wbase[m + n * M] = acc[mi][ni][r];
+                    }
+                }
+            }
+}
+
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const double* __restrict__ work,
+                                     double* C, int64_t ldc, double alpha, double beta) {
+    const int64_t total = M * N;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int sp = 0; sp < splits; ++sp) s += work[sp * total + i];
+        const int64_t m = i % M, n = i / M;
+        double* cp = C + m + n * ldc;
+        double v = alpha * s;
+        if (beta != 0.0) v += beta * *cp;
+        *cp = v;
+    }
+}
+
+__global__ void scale_kernel(int64_t M, int64_t N, double* C, int64_t ldc, double beta) {
+    const int64_t total = M * N;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t m = i % M, n = i / M;
+        double* cp = C + m + n * ldc;
+        *cp = beta == 0.0 ? 0.0 : beta * *cp;
+    }
+}
+
+namespace {
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, bool VEC>
+void launch_cfg(cudaStream_t stream, const GemmParams& p, int gx, int gy, int gz) {
+    using G = SmemGeom<BM, BN, BK, TA, TB>;
+    constexpr int smem = ST * (G::A_SZ + G::B_SZ) * static_cast<int>(sizeof(double));
+    constexpr int nt = (BM / WM) * (BN / WN) * 32;
+    auto kern = dgemm_kernel<BM, BN, BK, WM, WN, ST, TA, TB, VEC>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        RUTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = true;
+    }
+    kern<<<dim3(gx, gy, gz), nt, smem, stream>>>(p);
+    note_launch();
+    RUTV_CHECK_LAUNCH();
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST>
+void dispatch(cudaStream_t stream, const GemmParams& p, bool ta, bool tb, bool vec, int gz) {
+    const int gx = static_cast<int>((p.M + BM - 1) / BM), gy = static_cast<int>((p.N + BN - 1) / BN);
+#define RUTV_G(TA_, TB_, V_) \
+    launch_cfg<BM, BN, BK, WM, WN, ST, TA_, TB_, V_>(stream, p, gx, gy, gz)
+    if (vec) {
+        if (!ta && !tb) RUTV_G(false, false, true);
+        else if (!ta && tb) RUTV_G(false, true, true);
+        else if (ta && !tb) RUTV_G(true, false, true);
+        else RUTV_G(true, true, true);
+    } else {
+        if (!ta && !tb) RUTV_G(false, false, false);
+        else if (!ta && tb) RUTV_G(false, true, false);
+        else if (ta && !tb) RUTV_G(true, false, false);
+        else RUTV_G(true, true, false);
+    }
+#undef RUTV_G
+}
+
+inline bool aligned16(const void* ptr, int64_t ld) {
+    return (reinterpret_cast<uintptr_t>(ptr) % 16 == 0) && (ld % 2 == 0);
+}
+
+constexpr int kBK = 16;
+
+// Split-K factor for the small-tile config; 1 when the output tiles alone fill the chip.
+int choose_splits(int64_t M, int64_t N, int64_t K, int64_t work_elems) {
+    const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
+    const int64_t want_ctas = 3 * kNumSMs;
+    if (tiles >= want_ctas || K < 512) return 1;
+    int64_t sp = (want_ctas + tiles - 1) / tiles;
+    sp = std::min<int64_t>(sp, K / 256);
+    sp = std::min<int64_t>(sp, 32);
+    if (M * N > 0) sp = std::min<int64_t>(sp, work_elems / (M * N));
+    return static_cast<int>(std::max<int64_t>(sp, 1));
+}
+
+}  // namespace
+
+int64_t gemm_work_elems(int64_t m, int64_t n, int64_t k) {
+    const int sp = choose_splits(m, n, k, INT64_MAX / 4);
+    return sp > 1 ? sp * m * n : 0;
+}
+
+void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const DView& b,
+          double beta, const DView& c, double* work, int64_t work_elems) {
+    const int64_t opa_r = ta == Op::N ? a.rows : a.cols, opa_c = ta == Op::N ? a.cols : a.rows;
+    const int64_t opb_r = tb == Op::N ? b.rows : b.cols, opb_c = tb == Op::N ? b.cols : b.rows;
+    if (opa_c != opb_r || c.rows != opa_r || c.cols != opb_c)
+        throw Error(RUTV_ERR_SHAPE, "gemm shapes op(A)=" + std::to_string(opa_r) + "x" +
+                                        std::to_string(opa_c) + " op(B)=" + std::to_string(opb_r) +
+                                        "x" + std::to_string(opb_c) + " C=" +
+                                        std::to_string(c.rows) + "x" + std::to_string(c.cols));
+    const int64_t M = c.rows, N = c.cols, K = opa_c;
+    if (M == 0 || N == 0) return;
+    if (K == 0 || alpha == 0.0) {
+        if (beta != 1.0) {
+            scale_kernel<<<std::min<int64_t>((M * N + 255) / 256, 4 * kNumSMs), 256, 0, stream>>>(
+                M, N, c.data, c.ld, beta);
+            note_launch();
+            RUTV_CHECK_LAUNCH();
+        }
+        return;
+    }
+    GemmParams p{M, N, K, a.data, a.ld, b.data, b.ld, c.data, c.ld, alpha, beta, work, K, 1};
+    const bool vec = aligned16(a.data, a.ld) && aligned16(b.data, b.ld);
+    const bool tA = ta == Op::T, tB = tb == Op::T;
+    const int64_t tiles_l = ((M + 127) / 128) * ((N + 127) / 128);
+    if (tiles_l >= kNumSMs) {
+        dispatch<128, 128, kBK, 64, 32, 3>(stream, p, tA, tB, vec, 1);
+        return;
+    }
+    int splits = work ? choose_splits(M, N, K, work_elems) : 1;
+    if (splits > 1) {
+        int64_t kc = (K + splits - 1) / splits;
+        kc = (kc + kBK - 1) / kBK * kBK;
+        splits = static_cast<int>((K + kc - 1) / kc);
+        p.kchunk = kc;
+        p.splits = splits;
+    }
+    dispatch<64, 64, kBK, 32, 32, 3>(stream, p, tA, tB, vec, splits);
+    if (splits > 1) {
+        const int64_t total = M * N;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
+        splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(M, N, splits, work, c.data, c.ld, alpha,
+                                                         beta);
+        note_launch();
+        RUTV_CHECK_LAUNCH();
+    }
+}
+
+}  // namespace rutv

@@ -1,0 +1,133 @@
+// rutv_common.cuh -- shared definitions for the B200 randUTV kernels.
+//
+// All matrices are column-major FP64 with an explicit leading dimension,
+// element (i, j) at data[i + j*ld] -- the reference's storage contract
+// (proj/include/randutv/matrix.hpp:16-28), kept so device views map 1:1 onto
+// the reference's MatrixView sub-blocks.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/rutv_b200.h"
+
+namespace rutv {
+
+constexpr int kNumSMs = 148;  // B200; queried at runtime for sizing decisions
+
+// Error carrying a rutv status code; thrown inside the library, mapped to the
+// C-ABI status at the boundary (capi.cpp).
+struct Error : std::runtime_error {
+    int code;
+    double residual;
+    Error(int c, const std::string& msg, double r = 0.0)
+        : std::runtime_error(msg), code(c), residual(r) {}
+};
+
+#define RUTV_CUDA(x)                                                                  \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            throw ::rutv::Error(RUTV_ERR_CUDA, std::string("CUDA error ") +           \
+                                                   cudaGetErrorString(e_) + " at " +  \
+                                                   __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define RUTV_CHECK_LAUNCH() RUTV_CUDA(cudaGetLastError())
+
+// Non-owning device view (mirror of randutv::MatrixView, matrix.hpp:18-38).
+struct DView {
+    int64_t rows = 0, cols = 0, ld = 1;
+    double* data = nullptr;
+    DView() = default;
+    DView(int64_t r, int64_t c, int64_t l, double* d) : rows(r), cols(c), ld(l), data(d) {}
+    __host__ __device__ double* at(int64_t i, int64_t j) const { return data + i + j * ld; }
+    DView block(int64_t i0, int64_t j0, int64_t nr, int64_t nc) const {
+        if (i0 < 0 || j0 < 0 || nr < 0 || nc < 0 || i0 + nr > rows || j0 + nc > cols)
+            throw Error(RUTV_ERR_INDEX, "device subview out of range");
+        return DView(nr, nc, ld, data + i0 + j0 * ld);
+    }
+};
+
+enum class Op { N = 0, T = 1 };
+
+// Largest dynamic shared memory a kernel may request on this device, after its
+// static __shared__ usage (cudaDevAttrMaxSharedMemoryPerBlockOptin - static).
+inline int dyn_smem_cap(const void* kernel) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) return optin - 1024;
+    return optin - static_cast<int>(fa.sharedSizeBytes);
+}
+
+// ---- kernels' host launchers (all asynchronous on `stream`) ----
+
+// C <- alpha op(A) op(B) + beta C.  beta == 0 writes C without reading it, so
+// stale NaN never leaks (matrix_ops.hpp:9-18).  Deterministic: split-K partials
+// are reduced in a fixed order.  `work`/`work_elems` is scratch for split-K.
+void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const DView& b,
+          double beta, const DView& c, double* work, int64_t work_elems);
+// Scratch (in doubles) the gemm launcher may want for this shape.
+int64_t gemm_work_elems(int64_t m, int64_t n, int64_t k);
+// Count of kernels launched by this library since process start (bench evidence).
+uint64_t launch_count();
+void note_launch(int n = 1);
+
+// G(i, j) = normal_at(seed, pos + i + j*rows)  (proj/src/rng.cpp:29-53).
+void normal_fill(cudaStream_t stream, uint64_t seed, uint64_t pos, const DView& g);
+
+// Small elementwise kernels.
+void set_identity(cudaStream_t stream, const DView& a);
+void copy_view(cudaStream_t stream, const DView& dst, const DView& src);
+// W (rows x p) = unit-lower-trapezoidal reflector matrix of packed QR
+// (proj/src/householder.cpp:37-44).
+void make_w(cudaStream_t stream, const DView& qr, int64_t p, const DView& w);
+// block := rectangular diagonal of sigma, zeros elsewhere (randutv_blocked.cpp:32-37).
+void write_rect_diag(cudaStream_t stream, const DView& block, const double* sigma, int64_t p);
+// dst (rt x bw) = upper trapezoid of src, zeros below (randutv_blocked.cpp:73-75).
+void copy_upper(cudaStream_t stream, const DView& dst, const DView& src);
+
+// Householder panel QR (reference house() convention, householder.cpp:20-67)
+// of an s x w panel in place; tau[0..min(s,w)).  `scratch` holds sub-panel
+// workspace (see hqr_work_elems).
+void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, int64_t ldt,
+               double* scratch, int64_t scratch_elems);
+int64_t hqr_work_elems(int64_t s, int64_t w);
+// Twy from the Gram matrix of W and tau (householder.cpp:76-97).
+void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* tau, int64_t p,
+            double* t, int64_t ldt);
+
+// One-sided Jacobi SVD of a square block (jacobi_svd.cpp:39-148).  Writes U, sigma, V
+// (n x n, ld n).  Status (code, residual) is written to dev_status[0..1] on the
+// device; the caller checks it after synchronising.
+void svd_block(cudaStream_t stream, const DView& a, double* u, double* sigma, double* v,
+               double* work, int64_t work_elems, double* dev_status, double tol, int max_sweeps);
+int64_t svd_work_elems(int64_t n, int max_sweeps);
+
+// Arguments of the single-GPU driver (randutv.cu); all pointers are device.
+struct FactorArgs {
+    int64_t b;
+    int q;
+    bool build_u, build_v;
+    uint64_t seed;
+    int max_steps;
+    const double* dA;  // n x n, lda
+    int64_t lda;
+    const double* dG;  // host-stream G (parity mode) or null (device RNG)
+    double* dT;
+    int64_t ldt;
+    double* dU;        // may be null when !build_u
+    int64_t ldu;
+    double* dV;        // may be null when !build_v
+    int64_t ldv;
+};
+void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& fa);
+int last_profile(const char** names, double* ms, int cap);
+
+}  // namespace rutv
