@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""bench.py -- B200 blocked randUTV benchmark (BASELINE.json metric).
+
+Metric: randUTV FP64 effective GFLOP/s = F(n, b, q) / time, F the reference's
+algorithmic flop count (U and V built).
+Workload (BASELINE.json configs[1]): n = 4000 geometric A = Q1 diag(sigma) Q2^T,
+sigma_i = 10^(-12 (i-1)/(n-1)), b = 128, q = 2, full U, T, V.  A is built on
+the device with the reference's Haar construction (metrics.cpp:95-110) from a
+fixed seed -- synthetic data, no dataset involved.
+
+A "step" is one complete factorization of that matrix.
+  value : device-resident (A in HBM, outputs in HBM), CUDA events on the stream
+          the library runs on, max over ranks.
+  e2e   : the C-ABI host call rutv_b200_factorize with pinned host buffers:
+          H2D of A and D2H of T, U, V inside the timed region.
+Every input (A 128 MB, state 384 MB) exceeds the 126 MB L2, so no flush is
+needed between iterations.
+
+--impl reference: the reference's own CPU randUTV (oracle/_ref, compiled from
+/root/reference/proj/src unmodified), single-threaded as the reference is by
+contract, timed on a bounded sample of the same workload
+family: n = 1000, b = 128, q = 2, geometric sigma 1 -> 1e-12.
+
+--gpus N > 1 (torchrun): each rank factors its own matrix (independent
+replicas, weak scaling); the 2D block-cyclic sharded path is not wired into
+this bench yet.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEF, B_DEF, Q_DEF = 4000, 128, 2
+SEED_A, SEED_G = 1, 2
+DMMA_PEAK_TFLOPS = 37.1  # profiles/r01_dmma_peak.jsonl: mma.sync f64 burst, 148 SMs, 1.965 GHz
+METRIC = "randUTV FP64 effective GFLOP/s & time at 1/2/4/8 B200; % of FP64 TC peak"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def workload_name(n, b, q):
+    return f"config2: n={n} geometric sigma 1->1e-12, b={b}, q={q}, full U/T/V"
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# -------------------------------------------------------------- reference --
+def reference_sample(n=1000, b=B_DEF, q=Q_DEF):
+    """Time the unmodified reference randutv() (oracle/_ref) once on the sample."""
+    import oracle
+    a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A, impl="ref")
+    t0 = time.perf_counter()
+    oracle.randutv(a, b=b, q=q, seed=SEED_G, impl="ref")
+    dt = time.perf_counter() - t0
+    return oracle.flops(n, b, q) / dt / 1e9, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    if not oracle.available("ref"):
+        kind = "port"
+    else:
+        kind = "reference"
+    n = 1000
+    vals, times = [], []
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            v, dt = reference_sample(n)
+        else:  # the C restatement (only if the reference library is missing)
+            a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A)
+            t0 = time.perf_counter()
+            oracle.randutv(a, b=B_DEF, q=Q_DEF, seed=SEED_G)
+            dt = time.perf_counter() - t0
+            v = oracle.flops(n, B_DEF, Q_DEF) / dt / 1e9
+        if i >= args.warmup:
+            vals.append(v)
+            times.append(dt)
+    value = statistics.median(vals)
+    sample = (f"full factorization of an n={n} member of the config-2 family (b=128, q=2, geometric "
+              f"sigma 1->1e-12), reference randutv() single thread; value = F({n},128,2)/t")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * statistics.median(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(N_DEF, B_DEF, Q_DEF), "sample_n": n, "b": B_DEF,
+                   "q": Q_DEF, "parallelism": "cpu-1thread"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": 1, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- B200 --
+def cm(torch, m, n, dev):
+    return torch.empty((n, m), dtype=torch.float64, device=dev).T
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEF)
+    ap.add_argument("--b", type=int, default=B_DEF)
+    ap.add_argument("--q", type=int, default=Q_DEF)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2104_05782_b200 as rutv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, b, q = args.n, args.b, args.q
+    F = rutv.flops(n, b, q)
+
+    a = cm(torch, n, n, dev)
+    rutv.spectrum_matrix_device(a, SEED_A + rank, beta=10 ** (-12 / (n - 1)))
+    t, u, v = cm(torch, n, n, dev), cm(torch, n, n, dev), cm(torch, n, n, dev)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step():
+        rutv.factorize_device(a, t, u, v, b=b, q=q, seed=SEED_G, stream=sh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    launches0 = rutv.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = rutv.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    clocks = clk.summary()
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * F / (ms_max / 1e3) / 1e9
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        import numpy as np
+        ha = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        ha.copy_(a.T.cpu())  # column-major bytes of A
+        ht = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        hu = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        hv = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        o = rutv.make_opts(b=b, q=q, seed=SEED_G, device=local, stream=sh)
+        st = rutv.Status()
+        L = rutv.lib()
+
+        def e2e_step():
+            L.rutv_b200_factorize(C.byref(o), C.c_void_p(ha.data_ptr()), n, n, n, None, 0,
+                                  C.c_void_p(ht.data_ptr()), n, C.c_void_p(hu.data_ptr()), n,
+                                  C.c_void_p(hv.data_ptr()), n, C.byref(st))
+            rutv._raise(st)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * F / (float(ems.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "ms_per_step": round(float(ems.item()), 3),
+               "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 3 * 8 * n * n}
+        # sanity: the host result matches the device one (same stream of deviates)
+        assert np.allclose(ht.numpy().T[:4, :4], t.cpu().numpy()[:4, :4])
+
+    # ---- roofline of the dominant kernel (DMMA GEMM), separate profiled pass
+    os.environ["RUTV_GEMM_PROFILE"] = "1"
+    step()
+    torch.cuda.synchronize()
+    os.environ["RUTV_GEMM_PROFILE"] = "0"
+    gp = rutv.gemm_profile()
+    gemm_tflops = gp["flops"] / (gp["ms"] / 1e3) / 1e12 if gp["ms"] > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": round(gemm_tflops, 3) if gemm_tflops else None,
+                "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(gemm_tflops / DMMA_PEAK_TFLOPS, 4) if gemm_tflops else None,
+                "traffic": traffic, "kernel": "dgemm_kernel (+split-K reduce)",
+                "gemm_ms_per_step": round(gp["ms"], 3), "gemm_launches": gp["launches"],
+                "gemm_share_of_step": round(gp["ms"] / ms, 4) if ms > 0 else None,
+                "step_frac_of_peak": round(F / (ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS, 4),
+                "peak_source": "measured DMMA burst (profiles/r01_dmma_peak.jsonl); "
+                               "MEASURED_PEAKS.json has no FP64 entry"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            if oracle.available("ref"):
+                v_ref, dt = reference_sample(1000)
+                cpu = {"value": round(v_ref, 4), "unit": "GFLOP/s", "cores": 1, "kind": "reference",
+                       "sample": f"reference randutv() on n=1000 of the config-2 family "
+                                 f"(b=128, q=2, geometric), {dt:.2f} s, single thread"}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated Haar product, seed 1)",
+            "config": {"workload": workload_name(n, b, q), "n": n, "b": b, "q": q,
+                       "flops_per_step": F, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (A 128 MB + 384 MB state) exceed the 126 MB L2; no flush"},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

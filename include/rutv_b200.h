@@ -57,7 +57,9 @@ typedef struct {
     int32_t device;     /* CUDA device ordinal                               */
     int32_t max_steps;  /* < 0: run to completion; else stop after k steps   */
     int32_t overlap;    /* 1: off-critical-path updates on a second stream  */
-    int32_t reserved[7];
+    int32_t reserved0;
+    uint64_t stream;    /* cudaStream_t to run on (0: an internal stream)    */
+    int32_t reserved[4];
 } rutv_opts;
 
 /* Fills the reference defaults: b=128, q=1, build_u=build_v=1, seed=0,
@@ -101,6 +103,11 @@ int rutv_b200_last_profile(const char** names, double* ms, int cap);
 /* Kernels this library launched since load (evidence for bench.py). */
 uint64_t rutv_b200_launch_count(void);
 
+/* GEMM-kernel totals of the last factorize call on this thread when
+ * RUTV_GEMM_PROFILE=1 (CUDA events around every GEMM launch): algorithmic
+ * flops (2MNK), device ms, launch count.  Returns 0 when no data. */
+int rutv_b200_gemm_profile(double* flops, double* ms, int64_t* launches);
+
 /* ---------------- L1 kernels (DEVICE pointers, stream 0 of o->device) ---------------- */
 
 /* gemm (proj/src/gemm.cpp:21, contract matrix_ops.hpp:9-18):
@@ -132,6 +139,19 @@ int rutv_b200_svd_block(int device, const double* A, int64_t n, int64_t lda, dou
  * position pos, column-major. */
 int rutv_b200_normal_fill(int device, uint64_t seed, uint64_t pos, double* G, int64_t rows,
                           int64_t cols, int64_t ldg, rutv_status* st);
+
+/* ---------------- on-device test-matrix generators (metrics.cpp:90-110) ---------------- */
+
+/* gaussian_matrix: A(i, j) = RngState(seed).normal_at(i + j*m). DEVICE pointer. */
+int rutv_b200_gaussian_matrix(int device, int64_t m, int64_t n, uint64_t seed, double* A,
+                              int64_t lda, rutv_status* st);
+
+/* geometric_matrix / explicit spectrum: A = Q1 diag(sigma) Q2' with Haar Q1, Q2 built as
+ * form_q(hqr(G)) from one RngState(seed) (G1 m x p first, then G2 n x p).
+ * sigma: HOST array of min(m, n) values, or NULL for sigma_j = beta^j (accumulated
+ * s *= beta as metrics.cpp:103-106 does).  A: DEVICE pointer. */
+int rutv_b200_spectrum_matrix(int device, int64_t m, int64_t n, const double* sigma, double beta,
+                              uint64_t seed, double* A, int64_t lda, rutv_status* st);
 
 #ifdef __cplusplus
 }

@@ -50,7 +50,8 @@ class Status(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("b", C.c_int64), ("q", C.c_int32), ("build_u", C.c_int32), ("build_v", C.c_int32),
                 ("qr_prepass", C.c_int32), ("seed", C.c_uint64), ("device", C.c_int32),
-                ("max_steps", C.c_int32), ("overlap", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("max_steps", C.c_int32), ("overlap", C.c_int32), ("reserved0", C.c_int32),
+                ("stream", C.c_uint64), ("reserved", C.c_int32 * 4)]
 
 
 _D = C.POINTER(C.c_double)
@@ -80,6 +81,11 @@ def lib() -> C.CDLL:
     L.rutv_b200_factorize_device.argtypes = fac
     L.rutv_b200_last_profile.argtypes = [C.POINTER(C.c_char_p), _D, C.c_int]
     L.rutv_b200_launch_count.restype = C.c_uint64
+    L.rutv_b200_gemm_profile.argtypes = [_D, _D, C.POINTER(_I64)]
+    L.rutv_b200_gaussian_matrix.argtypes = [C.c_int, _I64, _I64, C.c_uint64, C.c_void_p, _I64,
+                                            C.POINTER(Status)]
+    L.rutv_b200_spectrum_matrix.argtypes = [C.c_int, _I64, _I64, C.c_void_p, C.c_double, C.c_uint64,
+                                            C.c_void_p, _I64, C.POINTER(Status)]
     L.rutv_b200_gemm.argtypes = [C.c_int, C.c_double, C.c_int, C.c_void_p, _I64, _I64, _I64, C.c_int,
                                  C.c_void_p, _I64, _I64, _I64, C.c_double, C.c_void_p, _I64, _I64,
                                  _I64, C.POINTER(Status)]
@@ -111,12 +117,13 @@ def _raise(st: Status) -> None:
 
 def make_opts(b: int = 128, q: int = 1, seed: int = 0, build_u: bool = True, build_v: bool = True,
               qr_prepass: bool = False, device: int = 0, max_steps: int = -1,
-              overlap: bool = True) -> Opts:
+              overlap: bool = True, stream: int = 0) -> Opts:
     o = Opts()
     lib().rutv_b200_default_opts(C.byref(o))
     o.b, o.q, o.seed = int(b), int(q), int(seed)
     o.build_u, o.build_v, o.qr_prepass = int(build_u), int(build_v), int(qr_prepass)
     o.device, o.max_steps, o.overlap = int(device), int(max_steps), int(overlap)
+    o.stream = int(stream)
     return o
 
 
@@ -168,7 +175,8 @@ def factorize(a, *, b: int = 0, q: int = 1, algo: str = "b200", seed: int = 0,
 
 
 def factorize_device(a, t, u=None, v=None, *, b: int = 128, q: int = 1, seed: int = 0,
-                     g=None, device: int | None = None, max_steps: int = -1) -> None:
+                     g=None, device: int | None = None, max_steps: int = -1,
+                     stream: int = 0) -> None:
     """Device-resident variant on torch CUDA tensors (column-major = a
     transposed contiguous row-major tensor; pass ``x.T`` views with stride (1, ld))."""
     def info(x):
@@ -179,7 +187,7 @@ def factorize_device(a, t, u=None, v=None, *, b: int = 128, q: int = 1, seed: in
     m, n = a.shape
     dev = a.device.index if device is None else device
     o = make_opts(b=b, q=q, seed=seed, build_u=u is not None, build_v=v is not None, device=dev,
-                  max_steps=max_steps)
+                  max_steps=max_steps, stream=stream)
     pa, lda = info(a)
     pt, ldt = info(t)
     pu, ldu = info(u)
@@ -264,4 +272,32 @@ def normal_fill(seed: int, pos: int, g) -> None:
     pg, r, c, ld = _cm(g)
     st = Status()
     lib().rutv_b200_normal_fill(g.device.index, seed, pos, pg, r, c, ld, C.byref(st))
+    _raise(st)
+
+
+def gemm_profile() -> dict:
+    """GEMM totals of the last factorize call (needs RUTV_GEMM_PROFILE=1)."""
+    f, ms, n = C.c_double(), C.c_double(), _I64()
+    lib().rutv_b200_gemm_profile(C.byref(f), C.byref(ms), C.byref(n))
+    return {"flops": f.value, "ms": ms.value, "launches": n.value}
+
+
+def gaussian_matrix_device(a, seed: int) -> None:
+    """gaussian_matrix (metrics.cpp:90-93) into a column-major CUDA tensor."""
+    pa, m, n, lda = _cm(a)
+    st = Status()
+    lib().rutv_b200_gaussian_matrix(a.device.index, m, n, seed, pa, lda, C.byref(st))
+    _raise(st)
+
+
+def spectrum_matrix_device(a, seed: int, sigma=None, beta: float = 1.0) -> None:
+    """Q1 diag(sigma) Q2^T with Haar factors (metrics.cpp:24-28, 95-110) on the device;
+    sigma=None gives geometric_matrix's beta^j."""
+    pa, m, n, lda = _cm(a)
+    sp = None
+    if sigma is not None:
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        sp = _ptr(sigma)
+    st = Status()
+    lib().rutv_b200_spectrum_matrix(a.device.index, m, n, sp, beta, seed, pa, lda, C.byref(st))
     _raise(st)

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "rutv_common.cuh"
 
@@ -57,9 +58,19 @@ void check_opts(const rutv_opts* o) {
 
 struct Stream {
     cudaStream_t s = nullptr;
+    bool owned = true;
     Stream() { RUTV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    // Caller-provided stream (rutv_opts::stream) when non-zero.
+    explicit Stream(uint64_t handle) {
+        if (handle) {
+            s = reinterpret_cast<cudaStream_t>(handle);
+            owned = false;
+        } else {
+            RUTV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        }
+    }
     ~Stream() {
-        if (s) cudaStreamDestroy(s);
+        if (s && owned) cudaStreamDestroy(s);
     }
 };
 
@@ -155,7 +166,7 @@ int rutv_b200_factorize(const rutv_opts* o, const double* A, int64_t m, int64_t 
     return guarded(st, [&] {
         check_opts(o);
         set_device(o->device);
-        Stream s;
+        Stream s(o->stream);
         const int64_t mm = std::max<int64_t>(m, 0), nn = std::max<int64_t>(n, 0);
         DMem<double> dA(static_cast<size_t>(mm * nn), s.s), dT(static_cast<size_t>(mm * nn), s.s);
         DMem<double> dU(o->build_u ? static_cast<size_t>(mm * mm) : 1, s.s);
@@ -196,7 +207,7 @@ int rutv_b200_factorize_device(const rutv_opts* o, const double* dA, int64_t m, 
     return guarded(st, [&] {
         check_opts(o);
         set_device(o->device);
-        Stream s;
+        Stream s(o->stream);
         run_factorize(o, dA, m, n, lda, dG, g_len, dT, ldt, dU, ldu, dV, ldv, s.s);
         RUTV_CUDA(cudaStreamSynchronize(s.s));
     });
@@ -207,6 +218,10 @@ int rutv_b200_last_profile(const char** names, double* ms, int cap) {
 }
 
 uint64_t rutv_b200_launch_count(void) { return rutv::launch_count(); }
+
+int rutv_b200_gemm_profile(double* flops, double* ms, int64_t* launches) {
+    return rutv::gemm_profile_get(flops, ms, launches);
+}
 
 int rutv_b200_gemm(int device, double alpha, int ta, const double* A, int64_t ar, int64_t ac,
                    int64_t lda, int tb, const double* B, int64_t br, int64_t bc, int64_t ldb,
@@ -307,6 +322,41 @@ int rutv_b200_normal_fill(int device, uint64_t seed, uint64_t pos, double* G, in
         set_device(device);
         Stream s;
         rutv::normal_fill(s.s, seed, pos, DView(rows, cols, ldg, G));
+        RUTV_CUDA(cudaStreamSynchronize(s.s));
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rutv_b200_gaussian_matrix(int device, int64_t m, int64_t n, uint64_t seed, double* A,
+                              int64_t lda, rutv_status* st) {
+    return guarded(st, [&] {
+        set_device(device);
+        Stream s;
+        rutv::normal_fill(s.s, seed, 0, DView(m, n, lda, A));
+        RUTV_CUDA(cudaStreamSynchronize(s.s));
+    });
+}
+
+int rutv_b200_spectrum_matrix(int device, int64_t m, int64_t n, const double* sigma, double beta,
+                              uint64_t seed, double* A, int64_t lda, rutv_status* st) {
+    return guarded(st, [&] {
+        const int64_t p = std::min(m, n);
+        if (!sigma && !(beta > 0.0)) throw Error(RUTV_ERR_CONFIG, "geometric_matrix: decay factor must be positive");
+        set_device(device);
+        Stream s;
+        std::vector<double> hs(static_cast<size_t>(std::max<int64_t>(p, 1)));
+        double acc = 1.0;
+        for (int64_t j = 0; j < p; ++j) {
+            hs[static_cast<size_t>(j)] = sigma ? sigma[j] : acc;
+            acc *= beta;
+        }
+        DMem<double> ds(static_cast<size_t>(std::max<int64_t>(p, 1)), s.s);
+        RUTV_CUDA(cudaMemcpyAsync(ds.p, hs.data(), static_cast<size_t>(std::max<int64_t>(p, 1)) * 8,
+                                  cudaMemcpyHostToDevice, s.s));
+        rutv::spectrum_matrix(s.s, m, n, ds.p, seed, DView(m, n, lda, A));
         RUTV_CUDA(cudaStreamSynchronize(s.s));
     });
 }

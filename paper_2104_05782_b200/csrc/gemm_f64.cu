@@ -19,6 +19,9 @@
 //     results are bit-reproducible run to run.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "rutv_common.cuh"
 
@@ -27,6 +30,72 @@ namespace rutv {
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
 void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+// Optional per-launch GEMM timing (RUTV_GEMM_PROFILE=1): CUDA events on the
+// launching stream around every gemm() call, algorithmic flops 2MNK.
+namespace {
+struct GemmProf {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // pairs
+    double flops_acc = 0.0;
+    double flops = 0.0, ms = 0.0;
+    int64_t launches = 0;
+};
+thread_local GemmProf g_gp;
+}  // namespace
+
+void gemm_profile_begin() {
+    const char* e = std::getenv("RUTV_GEMM_PROFILE");
+    g_gp.on = e && std::strcmp(e, "0") != 0;
+    g_gp.ev.clear();
+    g_gp.flops_acc = 0.0;
+}
+
+void gemm_profile_end() {
+    if (!g_gp.on) return;
+    if (!g_gp.ev.empty()) cudaEventSynchronize(g_gp.ev.back());
+    double ms = 0.0;
+    for (size_t i = 0; i + 1 < g_gp.ev.size(); i += 2) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, g_gp.ev[i], g_gp.ev[i + 1]);
+        ms += t;
+    }
+    for (auto e : g_gp.ev) cudaEventDestroy(e);
+    g_gp.flops = g_gp.flops_acc;
+    g_gp.ms = ms;
+    g_gp.launches = static_cast<int64_t>(g_gp.ev.size() / 2);
+    g_gp.ev.clear();
+    g_gp.on = false;
+}
+
+int gemm_profile_get(double* flops, double* ms, int64_t* launches) {
+    if (flops) *flops = g_gp.flops;
+    if (ms) *ms = g_gp.ms;
+    if (launches) *launches = g_gp.launches;
+    return g_gp.launches > 0 ? 1 : 0;
+}
+
+namespace {
+struct ProfScope {
+    cudaStream_t st;
+    bool on;
+    ProfScope(cudaStream_t s, double flops) : st(s), on(g_gp.on) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        g_gp.ev.push_back(e);
+        g_gp.flops_acc += flops;
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        g_gp.ev.push_back(e);
+    }
+};
+}  // namespace
 
 struct GemmParams {
     int64_t M, N, K;
@@ -359,6 +428,7 @@ void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const
         }
         return;
     }
+    ProfScope prof(stream, 2.0 * static_cast<double>(M) * N * K);
     GemmParams p{M, N, K, a.data, a.ld, b.data, b.ld, c.data, c.ld, alpha, beta, work, K, 1};
     const bool vec = aligned16(a.data, a.ld) && aligned16(b.data, b.ld);
     const bool tA = ta == Op::T, tB = tb == Op::T;

@@ -128,6 +128,7 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
     prof.st = st;
     for (int i = 0; i < P_N; ++i) prof.names.push_back(kPhaseNames[i]);
     prof.mark(P_START);
+    gemm_profile_begin();
 
     const bool bu = fa.build_u, bv = fa.build_v;
     const int64_t vr = bv ? n : 0;          // V rows on top of T in VT
@@ -294,6 +295,7 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
                                   cudaMemcpyDeviceToHost, st));
     RUTV_CUDA(cudaStreamSynchronize(st));
     prof.finish();
+    gemm_profile_end();
     if (prof.on) {
         t_prof_names = prof.names;
         t_prof_ms = prof.ms;

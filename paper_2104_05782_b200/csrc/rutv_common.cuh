@@ -78,6 +78,10 @@ int64_t gemm_work_elems(int64_t m, int64_t n, int64_t k);
 // Count of kernels launched by this library since process start (bench evidence).
 uint64_t launch_count();
 void note_launch(int n = 1);
+// RUTV_GEMM_PROFILE=1: events around each gemm() between begin and end.
+void gemm_profile_begin();
+void gemm_profile_end();
+int gemm_profile_get(double* flops, double* ms, int64_t* launches);
 
 // G(i, j) = normal_at(seed, pos + i + j*rows)  (proj/src/rng.cpp:29-53).
 void normal_fill(cudaStream_t stream, uint64_t seed, uint64_t pos, const DView& g);
@@ -109,6 +113,15 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
 void svd_block(cudaStream_t stream, const DView& a, double* u, double* sigma, double* v,
                double* work, int64_t work_elems, double* dev_status, double tol, int max_sweeps);
 int64_t svd_work_elems(int64_t n, int max_sweeps);
+
+// Leading ncols columns of Q = H_1...H_p from packed qr (householder.cpp:155-173).
+void form_q(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
+            double* scratch, int64_t scratch_elems);
+int64_t form_q_work_elems(int64_t m, int64_t ncols);
+// A = Q1 diag(sigma) Q2' with the reference's Haar construction (metrics.cpp:24-28, 95-110);
+// sigma_dev has min(m, n) entries on the device.
+void spectrum_matrix(cudaStream_t st, int64_t m, int64_t n, const double* sigma_dev, uint64_t seed,
+                     const DView& a);
 
 // Arguments of the single-GPU driver (randutv.cu); all pointers are device.
 struct FactorArgs {
