@@ -61,38 +61,67 @@ __global__ void copy_upper_kernel(int64_t rows, int64_t cols, double* d, int64_t
     }
 }
 
-// Twy (p x p, upper) from z-vectors = strictly-upper Gram W'W and tau.
-// One CTA; thread k owns row k of T.  For column j: T(j,j) = tau_j and
-// T(k,j) = -tau_j * sum_{l=k}^{j-1} T(k,l) * G(l,j) for k < j.  T(k,l) for
-// fixed l is contiguous in k, so the l-outer loop reads T coalesced.
-__global__ void __launch_bounds__(1024) form_t_kernel(const double* gram, int64_t ldg,
-                                                      const double* tau, int p, double* t,
-                                                      int64_t ldt) {
-    extern __shared__ double zs[];  // p
-    const int k = threadIdx.x;
-    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(p) * p; i += blockDim.x) {
+// Twy (p x p, upper) from the Gram matrix G = W'W and tau, blocked by 32:
+//   diagonal blocks: the reference recurrence T(k,j) = -tau_j sum_{l=k}^{j-1}
+//   T(k,l) G(l,j) (householder.cpp:84-95), one warp per block, lane k owning
+//   row k in registers;
+//   block column J: T(0:J0, J) = -T(0:J0, 0:J0) (G(0:J0, J) T_JJ), the
+//   standard two-block composition of compact-WY factors.
+// One CTA.  T lives in shared memory for p <= 128, else in the output buffer.
+__global__ void __launch_bounds__(1024) form_t_kernel(const double* __restrict__ gram, int64_t ldg,
+                                                      const double* __restrict__ tau, int p,
+                                                      double* t, int64_t ldt, int t_in_smem) {
+    extern __shared__ __align__(16) double fsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* Ts = t_in_smem ? fsm : t;
+    const int64_t ld = t_in_smem ? p : ldt;
+    double* Xs = fsm + (t_in_smem ? static_cast<size_t>(p) * p : 0);  // up to (p-32) x 32
+    const int nblk = (p + 31) / 32;
+    // zero the strictly-lower part
+    for (int64_t i = tid; i < static_cast<int64_t>(p) * p; i += blockDim.x) {
         const int64_t r = i % p, c = i / p;
-        if (r > c) t[r + c * ldt] = 0.0;
+        if (r > c) Ts[r + c * ld] = 0.0;
     }
-    for (int j = 0; j < p; ++j) {
-        for (int l = threadIdx.x; l < j; l += blockDim.x) zs[l] = gram[l + static_cast<int64_t>(j) * ldg];
-        __syncthreads();
-        const double tj = tau[j];
-        if (k < j) {
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int l = k;
-            for (; l + 3 < j; l += 4) {
-                s0 += t[k + static_cast<int64_t>(l) * ldt] * zs[l];
-                s1 += t[k + static_cast<int64_t>(l + 1) * ldt] * zs[l + 1];
-                s2 += t[k + static_cast<int64_t>(l + 2) * ldt] * zs[l + 2];
-                s3 += t[k + static_cast<int64_t>(l + 3) * ldt] * zs[l + 3];
-            }
-            for (; l < j; ++l) s0 += t[k + static_cast<int64_t>(l) * ldt] * zs[l];
-            t[k + static_cast<int64_t>(j) * ldt] = -tj * ((s0 + s1) + (s2 + s3));
+    // diagonal blocks
+    __syncthreads();
+    if (warp < nblk) {  // lane k owns row I0 + k of the diagonal block
+        const int I0 = warp * 32, bw = min(32, p - I0);
+        double* row = Ts + (I0 + lane);
+        for (int j = 0; j < bw; ++j) {
+            const double tj = tau[I0 + j];
+            const double* gcol = gram + I0 + static_cast<int64_t>(I0 + j) * ldg;
+            double s = 0.0;
+            for (int l = lane; l < j; ++l) s += row[static_cast<int64_t>(I0 + l) * ld] * gcol[l];
+            if (lane < j) row[static_cast<int64_t>(I0 + j) * ld] = -tj * s;
+            else if (lane == j) row[static_cast<int64_t>(I0 + j) * ld] = tj;
         }
-        if (k == j) t[k + static_cast<int64_t>(j) * ldt] = tj;
+    }
+    __syncthreads();
+    // off-diagonal block columns
+    for (int J = 1; J < nblk; ++J) {
+        const int J0 = J * 32, bw = min(32, p - J0);
+        const int cnt = J0 * bw;
+        for (int e = tid; e < cnt; e += blockDim.x) {  // X = G(0:J0, J) T_JJ
+            const int r = e % J0, c = e / J0;
+            double s = 0.0;
+            for (int l = 0; l <= c; ++l)
+                s += gram[r + static_cast<int64_t>(J0 + l) * ldg] * Ts[(J0 + l) + static_cast<int64_t>(J0 + c) * ld];
+            Xs[r + static_cast<size_t>(c) * J0] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < cnt; e += blockDim.x) {  // T(0:J0, J) = -T(0:J0, 0:J0) X
+            const int r = e % J0, c = e / J0;
+            double s = 0.0;
+            for (int m = r; m < J0; ++m) s += Ts[r + static_cast<int64_t>(m) * ld] * Xs[m + static_cast<size_t>(c) * J0];
+            Ts[r + static_cast<int64_t>(J0 + c) * ld] = -s;
+        }
         __syncthreads();
     }
+    if (t_in_smem)
+        for (int64_t i = tid; i < static_cast<int64_t>(p) * p; i += blockDim.x) {
+            const int64_t r = i % p, c = i / p;
+            t[r + c * ldt] = Ts[r + c * p];
+        }
 }
 
 }  // namespace
@@ -141,9 +170,17 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
             double* t, int64_t ldt) {
     if (p == 0) return;
     if (p > 1024) throw Error(RUTV_ERR_NOTIMPL, "form_t: block size above 1024");
-    const int threads = static_cast<int>(std::max<int64_t>(32, (p + 31) / 32 * 32));
-    form_t_kernel<<<1, threads, static_cast<size_t>(p) * sizeof(double), stream>>>(
-        gram, ldg, tau, static_cast<int>(p), t, ldt);
+    static int cap = 0;
+    if (!cap) {
+        cap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_kernel));
+        RUTV_CUDA(cudaFuncSetAttribute(form_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    }
+    const size_t xs = static_cast<size_t>(std::max<int64_t>(p - 32, 1)) * 32 * sizeof(double);
+    const size_t tsm = static_cast<size_t>(p) * p * sizeof(double);
+    const bool in_smem = tsm + xs <= static_cast<size_t>(cap);
+    if (!in_smem && xs > static_cast<size_t>(cap)) throw Error(RUTV_ERR_NOTIMPL, "form_t: block too large");
+    form_t_kernel<<<1, 1024, in_smem ? tsm + xs : xs, stream>>>(gram, ldg, tau, static_cast<int>(p), t, ldt,
+                                                                in_smem ? 1 : 0);
     note_launch();
     RUTV_CHECK_LAUNCH();
 }

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -47,7 +48,20 @@ int guarded(rutv_status* st, F&& f) {
     }
 }
 
-void set_device(int device) { RUTV_CUDA(cudaSetDevice(device)); }
+void set_device(int device) {
+    RUTV_CUDA(cudaSetDevice(device));
+    // Keep stream-ordered allocations in the pool between calls (no OS
+    // re-mapping on every call).
+    static bool done[64] = {};
+    if (device >= 0 && device < 64 && !done[device]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done[device] = true;
+    }
+}
 
 void check_opts(const rutv_opts* o) {
     if (!o) throw Error(RUTV_ERR_CONFIG, "null options");
@@ -105,7 +119,8 @@ void run_factorize(const rutv_opts* o, const double* dA, int64_t m, int64_t n, i
     if (dG && g_len < rutv_b200_stream_length(m, n, o->b))
         throw Error(RUTV_ERR_SHAPE, "explicit G shorter than the stream the factorization draws");
     rutv::FactorArgs fa{o->b,  o->q, o->build_u != 0, o->build_v != 0, o->seed, o->max_steps, dA, lda,
-                        dG,    dT,   ldt,             dU,             ldu,     dV,          ldv};
+                        dG,    dT,   ldt,             dU,             ldu,     dV,          ldv,
+                        o->overlap != 0};
     rutv::factorize_device(st, o->device, n, fa);
 }
 
@@ -303,7 +318,7 @@ int rutv_b200_svd_block(int device, const double* A, int64_t n, int64_t lda, dou
     return guarded(st, [&] {
         set_device(device);
         Stream s;
-        const int64_t we = rutv::svd_work_elems(n, max_sweeps);
+        const int64_t we = rutv::svd_work_elems(n, max_sweeps) + 16;
         DMem<double> w(static_cast<size_t>(we), s.s), stat(4, s.s);
         RUTV_CUDA(cudaMemsetAsync(stat.p, 0, 32, s.s));
         rutv::svd_block(s.s, DView(n, n, lda, const_cast<double*>(A)), U, sigma, V, w.p, we, stat.p, tol,
@@ -311,6 +326,9 @@ int rutv_b200_svd_block(int device, const double* A, int64_t n, int64_t lda, dou
         double hs[4];
         RUTV_CUDA(cudaMemcpyAsync(hs, stat.p, 32, cudaMemcpyDeviceToHost, s.s));
         RUTV_CUDA(cudaStreamSynchronize(s.s));
+        if (std::getenv("RUTV_DEBUG"))
+            std::fprintf(stderr, "[rutv] svd_block n=%lld code=%g residual=%g kept=%g sweeps=%g\n",
+                         static_cast<long long>(n), hs[0], hs[1], hs[2], hs[3]);
         if (hs[0] == RUTV_ERR_CONVERGENCE)
             throw Error(RUTV_ERR_CONVERGENCE, "jacobi sweeps exhausted", hs[1]);
     });

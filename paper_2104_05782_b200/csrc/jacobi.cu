@@ -1,26 +1,31 @@
-// jacobi.cu -- one-sided Jacobi SVD of a square b x b block on a CTA cluster.
+// jacobi.cu -- batched one-sided Jacobi SVD of square blocks on CTA clusters.
 //
 // Restates svd_block (proj/src/jacobi_svd.cpp:39-148) with the reference's
 // acceptance semantics, reordered for parallelism:
 //   * pair test: skip if ||b_p|| or ||b_q|| <= floor_col = 4 n eps ||A||_F,
 //     or |b_p.b_q| <= rel ||b_p|| ||b_q||, rel = max(tol, sqrt(n) eps)
-//     (jacobi_svd.cpp:55-72); rotation zeta/t/c/s exactly as :74-80;
-//   * converged when a full sweep rotates nothing, ConvergenceError with the
-//     worst remaining pair ratio after max_sweeps (:97-109);
-//   * sigma_j = ||b_j||, stable descending sort, U = B/sigma above the floor,
+//     (jacobi_svd.cpp:55-72); zeta / t / c / s exactly as :74-80;
+//   * converged when a full sweep rotates nothing; ConvergenceError carrying
+//     the worst remaining pair ratio after max_sweeps (:97-109);
+//   * sigma_j = ||b_j||, stable descending sort, U = B / sigma above the floor,
 //     deterministic orthonormal completion below it (:111-146, :198-240).
-// The cyclic row ordering p<q of the reference is replaced by the round-robin
-// (circle) tournament ordering: each sweep is n-1 rounds of n/2 disjoint
-// pairs that are processed concurrently.  Rows of B (and V) are distributed
-// over a cluster of CS CTAs, resident in shared memory; per round the pair
-// partial sums (alpha, beta, gamma) are reduce-scattered to the pair's owner
-// CTA over DSMEM, the owner decides the rotation, and broadcasts (c, s) back:
-// two cluster barriers per round, O(n) DSMEM words per CTA.  Reductions are in
-// fixed rank order, so every CTA takes bit-identical decisions.
+// The reference's cyclic p<q order becomes the round-robin (circle)
+// tournament: a sweep is N-1 rounds of N/2 disjoint pairs processed at once.
+//
+// Layout: one cluster of CS CTAs per problem, many problems per launch (the
+// driver batches every b x b block of a factorization into one launch).  The
+// problem's rows are split over the cluster, B and V resident in shared
+// memory (V in a global work buffer when it does not fit).  A pair is owned by
+// a group of LPP = 8 lanes; each lane holds <= RPL rows of b_p, b_q in
+// registers, the three partial dots are reduced inside the 8-lane group, and
+// -- for CS > 1 -- exchanged over DSMEM (every CTA receives every pair's
+// partials, sums them in rank order, and takes the identical decision).  Per
+// round: one cluster barrier (or none for CS = 1) and one __syncthreads.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cfloat>
+#include <vector>
 
 #include "rutv_common.cuh"
 
@@ -31,7 +36,9 @@ namespace rutv {
 namespace {
 
 constexpr int kJThreads = 512;
-int kJSmemCap = 227 * 1024 - 1024;  // refined at first use (dyn_smem_cap)
+constexpr int kLPP = 8;                      // lanes per pair
+constexpr int kPPW = 32 / kLPP;              // pairs per warp
+constexpr int kPairsPerPass = kPPW * kJThreads / 32;  // 64
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -40,317 +47,326 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Round-robin pairing: N even players, round r in [0, N-1), pair pi in [0, N/2).
-__device__ __forceinline__ void rr_pair(int N, int r, int pi, int& x, int& y) {
-    auto pos = [&](int k) { return k == 0 ? 0 : 1 + ((k - 1 + r) % (N - 1)); };
-    x = pos(pi);
-    y = pos(N - 1 - pi);
+__device__ __forceinline__ void rr_pair(int N, int r, int pi, int& p, int& q) {
+    auto pos = [&](int k) {
+        if (k == 0) return 0;
+        int v = k - 1 + r;
+        if (v >= N - 1) v -= N - 1;
+        return 1 + v;
+    };
+    const int x = pos(pi), y = pos(N - 1 - pi);
+    p = min(x, y);
+    q = max(x, y);
 }
 
-struct JParams {
-    const double* A;
-    int64_t lda;
-    int n, N, R, npairs;
-    double* U;       // n x n, ld n
-    double* sigma;   // n
-    double* V;       // n x n, ld n
-    double* vglob;   // per-CTA V chunks in global memory when not in smem (else null)
-    double* gscr;    // global scratch: CS * max(n, 4) doubles
-    double tol;
-    int max_sweeps;
-    double* status;  // [code, residual, kept, sweeps]
-};
-
-__global__ void __launch_bounds__(kJThreads, 1) jacobi_kernel(const JParams P) {
+template <int RPL>
+__global__ void __launch_bounds__(kJThreads, 1)
+    jacobi_kernel(const SvdDesc* __restrict__ descs, int R, int vsm, double tol, int max_sweeps) {
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = static_cast<int>(cluster.num_blocks());
     const int rank = static_cast<int>(cluster.block_rank());
-    const int n = P.n, N = P.N, R = P.R, npairs = P.npairs;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int slots = (npairs + CS - 1) / CS;  // pairs owned per CTA
-
-    extern __shared__ __align__(16) double sm[];
-    double* Bs = sm;                                     // n columns x R rows
-    double* Vs = P.vglob ? P.vglob + static_cast<size_t>(rank) * n * R : Bs + static_cast<size_t>(n) * R;
-    double* part = (P.vglob ? Bs + static_cast<size_t>(n) * R : Vs + static_cast<size_t>(n) * R);  // 3*npairs
-    double* msg1 = part + 3 * npairs;                    // [CS][slots][3]
-    double* dec = msg1 + 3 * CS * slots;                 // [npairs][3] = c, s, flag
-    __shared__ int s_rot;
-    __shared__ double s_nf;
-    __shared__ double s_wp[kJThreads / 32];
-
+    const SvdDesc d = descs[blockIdx.x / CS];
+    const int n = d.n, N = n + (n & 1), npairs = N / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kJThreads / 32;
+    const int grp = lane / kLPP, sl = lane % kLPP;
     const int r_beg = rank * R;
     const int r_cnt = max(0, min(n, r_beg + R) - r_beg);
 
-    // load rows, V := I rows; ||A||_F partial
+    extern __shared__ __align__(16) double sm[];
+    double* Bs = sm;  // n columns x R rows
+    double* Vs = vsm ? Bs + static_cast<size_t>(n) * R : d.work + static_cast<size_t>(rank) * n * R;
+    double* xb = (vsm ? Vs : Bs) + static_cast<size_t>(n) * R;  // [2][CS][npairs][3]
+    const size_t xpar = static_cast<size_t>(CS) * npairs * 3;
+    __shared__ int s_rot;
+    __shared__ double s_red[32];
+
+    // load my rows of B, V := I rows, ||A||_F partial
     double fro = 0.0;
-    for (int idx = tid; idx < n * R; idx += blockDim.x) {
-        const int c = idx / R, r = idx % R;
-        double v = 0.0;
-        if (r < r_cnt) v = P.A[(r_beg + r) + static_cast<int64_t>(c) * P.lda];
-        Bs[idx] = v;
-        Vs[idx] = (r < r_cnt && r_beg + r == c) ? 1.0 : 0.0;
-        fro += v * v;
-    }
+    for (int c = 0; c < n; ++c)
+        for (int i = tid; i < R; i += kJThreads) {
+            double v = 0.0;
+            if (i < r_cnt) v = d.A[(r_beg + i) + static_cast<int64_t>(c) * d.lda];
+            Bs[static_cast<size_t>(c) * R + i] = v;
+            Vs[static_cast<size_t>(c) * R + i] = (i < r_cnt && r_beg + i == c) ? 1.0 : 0.0;
+            fro += v * v;
+        }
     fro = warp_sum(fro);
-    if (lane == 0) s_wp[warp] = fro;
+    if (lane == 0) s_red[warp] = fro;
     __syncthreads();
     if (tid == 0) {
         double s = 0.0;
-        for (int w = 0; w < nwarps; ++w) s += s_wp[w];
-        P.gscr[rank] = s;
+        for (int w = 0; w < nwarps; ++w) s += s_red[w];
+        if (CS > 1)
+            for (int dst = 0; dst < CS; ++dst) cluster.map_shared_rank(xb, dst)[rank] = s;
+        else
+            xb[0] = s;
     }
-    cluster.sync();
-    if (tid == 0) {
-        double s = 0.0;
-        for (int r = 0; r < CS; ++r) s += P.gscr[r];
-        s_nf = sqrt(s);
-    }
-    __syncthreads();
-    const double nf = s_nf;
+    if (CS > 1) cluster.sync(); else __syncthreads();
+    double nf2 = 0.0;
+    for (int r = 0; r < CS; ++r) nf2 += xb[r];
+    const double nf = sqrt(nf2);
     const double eps = DBL_EPSILON;
-    const double rel = fmax(P.tol, sqrt(static_cast<double>(n)) * eps);
+    const double rel = fmax(tol, sqrt(static_cast<double>(n)) * eps);
     const double floor_col = 4.0 * static_cast<double>(n) * eps * nf;
+    if (CS > 1) cluster.sync(); else __syncthreads();  // xb reused below
 
     if (n == 0 || nf == 0.0) {  // jacobi_svd.cpp:47-53: U = I, sigma = 0, V = I
-        for (int idx = tid; idx < n * r_cnt; idx += blockDim.x) {
-            const int c = idx / r_cnt, r = r_beg + idx % r_cnt;
-            P.U[r + static_cast<int64_t>(c) * n] = r == c ? 1.0 : 0.0;
-            P.V[r + static_cast<int64_t>(c) * n] = r == c ? 1.0 : 0.0;
-        }
+        for (int c = 0; c < n; ++c)
+            for (int i = tid; i < r_cnt; i += kJThreads) {
+                const int row = r_beg + i;
+                d.U[row + static_cast<int64_t>(c) * n] = row == c ? 1.0 : 0.0;
+                d.V[row + static_cast<int64_t>(c) * n] = row == c ? 1.0 : 0.0;
+            }
         if (rank == 0)
-            for (int j = tid; j < n; j += blockDim.x) P.sigma[j] = 0.0;
+            for (int j = tid; j < n; j += kJThreads) d.sigma[j] = 0.0;
         if (rank == 0 && tid == 0) {
-            P.status[0] = 0.0;
-            P.status[1] = 0.0;
-            P.status[2] = n;
-            P.status[3] = 0;
+            d.status[0] = 0.0;
+            d.status[1] = 0.0;
+            d.status[2] = n;
+            d.status[3] = 0;
         }
-        cluster.sync();
+        if (CS > 1) cluster.sync();
         return;
     }
 
-    // One round: partial dots -> owner reduce/decide -> broadcast -> rotate.
-    // check_only: no rotation; owners accumulate the worst ratio instead.
-    auto round = [&](int r, bool check_only, double& worst) {
-        for (int pi = warp; pi < npairs; pi += nwarps) {
-            int x, y;
-            rr_pair(N, r, pi, x, y);
+    // Phase 1 of a round: partial (alpha, beta, gamma) of every pair over my rows.
+    auto phase1 = [&](int r, int par) {
+        for (int base = 0; base < npairs; base += kPairsPerPass) {
+            const int pi = base + warp * kPPW + grp;
+            int p = 0, q = 0;
+            const bool ok = pi < npairs;
+            if (ok) rr_pair(N, r, pi, p, q);
+            const bool real = ok && q < n;
             double a = 0.0, b = 0.0, g = 0.0;
-            if (x < n && y < n) {
-                const int p = min(x, y), q = max(x, y);
+            if (real) {
                 const double* cp = Bs + static_cast<size_t>(p) * R;
                 const double* cq = Bs + static_cast<size_t>(q) * R;
-                for (int i = lane; i < r_cnt; i += 32) {
-                    const double u = cp[i], v = cq[i];
-                    a += u * u;
-                    b += v * v;
-                    g += u * v;
+#pragma unroll
+                for (int t = 0; t < RPL; ++t) {
+                    const int i = sl + kLPP * t;
+                    if (i < r_cnt) {
+                        const double u = cp[i], v = cq[i];
+                        a += u * u;
+                        b += v * v;
+                        g += u * v;
+                    }
                 }
-                a = warp_sum(a);
-                b = warp_sum(b);
-                g = warp_sum(g);
             }
-            if (lane == 0) {
-                double* dst = CS > 1 ? cluster.map_shared_rank(msg1, pi % CS) : msg1;
-                double* slot = dst + 3 * (rank * slots + pi / CS);
-                slot[0] = a;
-                slot[1] = b;
-                slot[2] = g;
+#pragma unroll
+            for (int o = kLPP / 2; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+                g += __shfl_xor_sync(0xffffffffu, g, o);
+            }
+            if (ok) {
+                if (CS == 1) {
+                    if (sl == 0) {
+                        double* slot = xb + par * xpar + static_cast<size_t>(pi) * 3;
+                        slot[0] = a;
+                        slot[1] = b;
+                        slot[2] = g;
+                    }
+                } else {
+                    for (int dst = sl; dst < CS; dst += kLPP) {
+                        double* slot = cluster.map_shared_rank(xb, dst) + par * xpar +
+                                       (static_cast<size_t>(rank) * npairs + pi) * 3;
+                        slot[0] = a;
+                        slot[1] = b;
+                        slot[2] = g;
+                    }
+                }
             }
         }
-        if (CS > 1) cluster.sync(); else __syncthreads();
-        // owner: pairs pi = rank + k*CS
-        for (int k = tid; k < slots; k += blockDim.x) {
-            const int pi = rank + k * CS;
-            if (pi >= npairs) continue;
-            int x, y;
-            rr_pair(N, r, pi, x, y);
-            double c = 1.0, s = 0.0, flag = 0.0;
-            if (x < n && y < n) {
+    };
+
+    bool converged = false;
+    int sweep = 0;
+    int par = 0;
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+        if (tid == 0) s_rot = 0;
+        for (int r = 0; r < N - 1; ++r, par ^= 1) {
+            phase1(r, par);
+            if (CS > 1) cluster.sync(); else __syncthreads();
+            bool any = false;
+            for (int base = 0; base < npairs; base += kPairsPerPass) {
+                const int pi = base + warp * kPPW + grp;
+                if (pi >= npairs) continue;
+                int p, q;
+                rr_pair(N, r, pi, p, q);
+                if (q >= n) continue;
                 double al = 0.0, be = 0.0, ga = 0.0;
                 for (int rr = 0; rr < CS; ++rr) {
-                    const double* slot = msg1 + 3 * (rr * slots + k);
+                    const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
                     al += slot[0];
                     be += slot[1];
                     ga += slot[2];
                 }
                 const double np = sqrt(al), nq = sqrt(be);
-                if (!(np <= floor_col || nq <= floor_col)) {
-                    if (check_only) {
-                        worst = fmax(worst, fabs(ga) / (np * nq));
-                    } else if (!(fabs(ga) <= rel * np * nq)) {
-                        const double zeta = (be - al) / (2.0 * ga);
-                        const double t = (zeta >= 0.0 ? 1.0 : -1.0) /
-                                         (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = c * t;
-                        flag = 1.0;
+                if (np <= floor_col || nq <= floor_col) continue;
+                if (fabs(ga) <= rel * np * nq) continue;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + tt * tt);
+                const double s = c * tt;
+                any = true;
+                double* bp = Bs + static_cast<size_t>(p) * R;
+                double* bq = Bs + static_cast<size_t>(q) * R;
+                double* vp = Vs + static_cast<size_t>(p) * R;
+                double* vq = Vs + static_cast<size_t>(q) * R;
+#pragma unroll
+                for (int t = 0; t < RPL; ++t) {
+                    const int i = sl + kLPP * t;
+                    if (i < r_cnt) {
+                        const double x = bp[i], y = bq[i], vx = vp[i], vy = vq[i];
+                        bp[i] = c * x - s * y;
+                        bq[i] = s * x + c * y;
+                        vp[i] = c * vx - s * vy;
+                        vq[i] = s * vx + c * vy;
                     }
                 }
             }
-            for (int d = 0; d < CS; ++d) {
-                double* dd = (CS > 1 ? cluster.map_shared_rank(dec, d) : dec) + 3 * pi;
-                dd[0] = c;
-                dd[1] = s;
-                dd[2] = flag;
-            }
+            if (any) s_rot = 1;
+            __syncthreads();
         }
-        if (CS > 1) cluster.sync(); else __syncthreads();
-        if (check_only) return;
-        // rotate my rows of B and V: pair-major, rows fastest
-        const int work = npairs * r_cnt;
-        for (int idx = tid; idx < work; idx += blockDim.x) {
-            const int pi = idx / r_cnt, i = idx - pi * r_cnt;
-            const double* dd = dec + 3 * pi;
-            if (dd[2] == 0.0) continue;
-            int x, y;
-            rr_pair(N, r, pi, x, y);
-            const int p = min(x, y), q = max(x, y);
-            const double c = dd[0], s = dd[1];
-            double* bp = Bs + static_cast<size_t>(p) * R + i;
-            double* bq = Bs + static_cast<size_t>(q) * R + i;
-            const double u = *bp, v = *bq;
-            *bp = c * u - s * v;
-            *bq = s * u + c * v;
-            double* vp = Vs + static_cast<size_t>(p) * R + i;
-            double* vq = Vs + static_cast<size_t>(q) * R + i;
-            const double vu = *vp, vv = *vq;
-            *vp = c * vu - s * vv;
-            *vq = s * vu + c * vv;
-        }
-        if (tid < npairs && dec[3 * tid + 2] != 0.0) s_rot = 1;
-        __syncthreads();
-    };
-
-    bool converged = false;
-    int sweep = 0;
-    double dummy = 0.0;
-    for (; sweep < P.max_sweeps && !converged; ++sweep) {
-        if (tid == 0) s_rot = 0;
-        __syncthreads();
-        for (int r = 0; r < N - 1; ++r) round(r, false, dummy);
         converged = s_rot == 0;
         __syncthreads();
     }
-    if (!converged) {
+
+    if (!converged) {  // residual: worst remaining pair ratio (jacobi_svd.cpp:97-109)
         double worst = 0.0;
-        for (int r = 0; r < N - 1; ++r) round(r, true, worst);
-        // owners' local maxima -> global scratch -> max
-        __shared__ double s_w[kJThreads / 32];
-        double wmax = worst;
-        for (int o = 16; o > 0; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-        if (lane == 0) s_w[warp] = wmax;
-        __syncthreads();
-        if (tid == 0) {
-            double m = 0.0;
-            for (int w = 0; w < nwarps; ++w) m = fmax(m, s_w[w]);
-            P.gscr[rank] = m;
+        for (int r = 0; r < N - 1; ++r, par ^= 1) {
+            phase1(r, par);
+            if (CS > 1) cluster.sync(); else __syncthreads();
+            for (int base = 0; base < npairs; base += kPairsPerPass) {
+                const int pi = base + warp * kPPW + grp;
+                if (pi >= npairs) continue;
+                int p, q;
+                rr_pair(N, r, pi, p, q);
+                if (q >= n) continue;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int rr = 0; rr < CS; ++rr) {
+                    const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
+                    al += slot[0];
+                    be += slot[1];
+                    ga += slot[2];
+                }
+                const double np = sqrt(al), nq = sqrt(be);
+                if (!(np <= floor_col || nq <= floor_col)) worst = fmax(worst, fabs(ga) / (np * nq));
+            }
+            __syncthreads();
         }
-        cluster.sync();
+        for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+        if (lane == 0) s_red[warp] = worst;
+        __syncthreads();
         if (rank == 0 && tid == 0) {
             double m = 0.0;
-            for (int r = 0; r < CS; ++r) m = fmax(m, P.gscr[r]);
-            P.status[0] = RUTV_ERR_CONVERGENCE;
-            P.status[1] = m;
-            P.status[2] = n;
-            P.status[3] = sweep;
+            for (int w = 0; w < nwarps; ++w) m = fmax(m, s_red[w]);
+            d.status[0] = RUTV_ERR_CONVERGENCE;
+            d.status[1] = m;
+            d.status[2] = n;
+            d.status[3] = sweep;
         }
-        cluster.sync();
+        if (CS > 1) cluster.sync();
         return;
     }
 
-    // sigma_j = ||b_j||: partial column sums -> global scratch -> rank-order sum
+    // sigma_j = ||b_j||: partial column sums, all-gathered, summed in rank order.
+    if (CS > 1) cluster.sync();  // every CTA done reading xb
     for (int c = warp; c < n; c += nwarps) {
         const double* cc = Bs + static_cast<size_t>(c) * R;
         double a = 0.0;
         for (int i = lane; i < r_cnt; i += 32) a += cc[i] * cc[i];
         a = warp_sum(a);
-        if (lane == 0) P.gscr[static_cast<size_t>(rank) * n + c] = a;
+        if (lane < CS) {
+            double* dst = CS > 1 ? cluster.map_shared_rank(xb, lane) : xb;
+            dst[static_cast<size_t>(rank) * n + c] = a;
+        }
     }
-    cluster.sync();
-    double* sig = part;  // reuse: n <= 3*npairs
-    for (int c = tid; c < n; c += blockDim.x) {
+    if (CS > 1) cluster.sync(); else __syncthreads();
+    __shared__ double s_sig[1024];
+    __shared__ int s_dest[1024];
+    for (int c = tid; c < n; c += kJThreads) {
         double a = 0.0;
-        for (int r = 0; r < CS; ++r) a += P.gscr[static_cast<size_t>(r) * n + c];
-        sig[c] = sqrt(a);
+        for (int r = 0; r < CS; ++r) a += xb[static_cast<size_t>(r) * n + c];
+        s_sig[c] = sqrt(a);
     }
     __syncthreads();
-    // stable descending rank: t(j) = #{k: s_k > s_j} + #{k < j: s_k == s_j}
-    int* dest = reinterpret_cast<int*>(msg1);  // n ints fit in 3*CS*slots doubles
-    for (int j = tid; j < n; j += blockDim.x) {
-        const double sj = sig[j];
+    for (int j = tid; j < n; j += kJThreads) {  // stable descending rank
+        const double sj = s_sig[j];
         int t = 0;
         for (int k = 0; k < n; ++k) {
-            const double sk = sig[k];
+            const double sk = s_sig[k];
             t += (sk > sj) || (k < j && sk == sj);
         }
-        dest[j] = t;
+        s_dest[j] = t;
     }
     __syncthreads();
-    for (int idx = tid; idx < n * r_cnt; idx += blockDim.x) {
-        const int j = idx / r_cnt, i = idx - j * r_cnt;
-        const int t = dest[j];
-        const double s = sig[j];
-        const int64_t row = r_beg + i;
-        P.V[row + static_cast<int64_t>(t) * n] = Vs[static_cast<size_t>(j) * R + i];
-        P.U[row + static_cast<int64_t>(t) * n] =
-            s > floor_col ? Bs[static_cast<size_t>(j) * R + i] / s : 0.0;
-    }
-    if (rank == 0) {
-        for (int j = tid; j < n; j += blockDim.x) P.sigma[dest[j]] = sig[j];
-        if (tid == 0) {
-            int kept = 0;
-            for (int j = 0; j < n; ++j) kept += sig[j] > floor_col;
-            P.status[0] = 0.0;
-            P.status[1] = 0.0;
-            P.status[2] = kept;
-            P.status[3] = sweep;
+    for (int j = 0; j < n; ++j) {
+        const int t = s_dest[j];
+        const double s = s_sig[j];
+        for (int i = tid; i < r_cnt; i += kJThreads) {
+            const int64_t row = r_beg + i;
+            d.V[row + static_cast<int64_t>(t) * n] = Vs[static_cast<size_t>(j) * R + i];
+            d.U[row + static_cast<int64_t>(t) * n] =
+                s > floor_col ? Bs[static_cast<size_t>(j) * R + i] / s : 0.0;
         }
     }
-    cluster.sync();
+    if (rank == 0) {
+        for (int j = tid; j < n; j += kJThreads) d.sigma[s_dest[j]] = s_sig[j];
+        if (tid == 0) {
+            int kept = 0;
+            for (int j = 0; j < n; ++j) kept += s_sig[j] > floor_col;
+            d.status[0] = 0.0;
+            d.status[1] = 0.0;
+            d.status[2] = kept;
+            d.status[3] = sweep;
+        }
+    }
+    if (CS > 1) cluster.sync();
 }
 
 // complete_orthonormal (jacobi_svd.cpp:198-240) on U's columns kept..n-1: identity
 // candidates in index order, two Gram-Schmidt passes, accept norm > 0.25.
-// Rare path (rank-deficient blocks); one CTA, sequential over candidates.
-__global__ void complete_kernel(double* U, int n, const double* status, double* cand) {
-    const int kept = static_cast<int>(status[2]);
-    if (status[0] != 0.0 || kept >= n) return;
+// Rare path (rank-deficient blocks); one CTA per problem, early exit otherwise.
+__global__ void complete_kernel(const SvdDesc* __restrict__ descs) {
+    const SvdDesc d = descs[blockIdx.x];
+    const int n = d.n;
+    const int kept = static_cast<int>(d.status[2]);
+    if (d.status[0] != 0.0 || kept >= n) return;
+    double* U = d.U;
+    double* cand = d.work + static_cast<size_t>(n) * n;
     __shared__ double red[32];
     __shared__ double s_val;
+    const int nw = blockDim.x >> 5;
+    auto block_sum = [&](double v) {
+        v = warp_sum(v);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += red[w];
+            s_val = s;
+        }
+        __syncthreads();
+        const double r = s_val;
+        __syncthreads();
+        return r;
+    };
     int have = kept;
     for (int c = 0; c < n && have < n; ++c) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) cand[i] = i == c ? 1.0 : 0.0;
         __syncthreads();
         for (int pass = 0; pass < 2; ++pass)
             for (int j = 0; j < have; ++j) {
-                double d = 0.0;
-                for (int i = threadIdx.x; i < n; i += blockDim.x) d += U[i + static_cast<int64_t>(j) * n] * cand[i];
-                d = warp_sum(d);
-                if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    double s = 0.0;
-                    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-                    s_val = s;
-                }
-                __syncthreads();
-                const double dot = s_val;
+                double dd = 0.0;
+                for (int i = threadIdx.x; i < n; i += blockDim.x) dd += U[i + static_cast<int64_t>(j) * n] * cand[i];
+                const double dot = block_sum(dd);
                 for (int i = threadIdx.x; i < n; i += blockDim.x) cand[i] -= dot * U[i + static_cast<int64_t>(j) * n];
                 __syncthreads();
             }
         double nn = 0.0;
         for (int i = threadIdx.x; i < n; i += blockDim.x) nn += cand[i] * cand[i];
-        nn = warp_sum(nn);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nn;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-            s_val = sqrt(s);
-        }
-        __syncthreads();
-        const double nrm = s_val;
+        const double nrm = sqrt(block_sum(nn));
         if (nrm > 0.25) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) U[i + static_cast<int64_t>(have) * n] = cand[i] / nrm;
             ++have;
@@ -359,104 +375,119 @@ __global__ void complete_kernel(double* U, int n, const double* status, double* 
     }
 }
 
-int g_jmax_cluster = 0;
+struct JCfg {
+    int cs, R, vsm, rpl;
+    size_t smem;
+};
 
-int jmax_cluster() {
-    if (g_jmax_cluster) return g_jmax_cluster;
-    kJSmemCap = dyn_smem_cap(reinterpret_cast<const void*>(jacobi_kernel));
-    RUTV_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    RUTV_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kJSmemCap));
-    int best = 8;
-    for (int cs : {16, 8}) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(cs);
-        cfg.blockDim = dim3(kJThreads);
-        cfg.dynamicSmemBytes = kJSmemCap;
-        cudaLaunchAttribute attr;
-        attr.id = cudaLaunchAttributeClusterDimension;
-        attr.val.clusterDim.x = cs;
-        attr.val.clusterDim.y = 1;
-        attr.val.clusterDim.z = 1;
-        cfg.attrs = &attr;
-        cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, jacobi_kernel, &cfg) == cudaSuccess && nclusters > 0) {
-            best = cs;
-            break;
-        }
-        cudaGetLastError();
-    }
-    g_jmax_cluster = best;
-    return best;
+int g_jcap = 0, g_jmax_cluster = 0;
+
+template <int RPL>
+void prep_kernel() {
+    auto k = jacobi_kernel<RPL>;
+    RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g_jcap));
 }
 
-size_t jsmem(int n, int R, int cs, bool v_in_smem) {
-    const int N = n + (n & 1), npairs = N / 2, slots = (npairs + cs - 1) / cs;
-    return (static_cast<size_t>(n) * R * (v_in_smem ? 2 : 1) + 3 * npairs + 3 * cs * slots +
-            3 * npairs) * sizeof(double);
+void jinit() {
+    if (g_jcap) return;
+    g_jcap = dyn_smem_cap(reinterpret_cast<const void*>(jacobi_kernel<16>));
+    prep_kernel<2>();
+    prep_kernel<4>();
+    prep_kernel<8>();
+    prep_kernel<16>();
+    g_jmax_cluster = 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(kJThreads);
+    cfg.dynamicSmemBytes = g_jcap;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 16;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, jacobi_kernel<16>, &cfg) == cudaSuccess && ncl > 0)
+        g_jmax_cluster = 16;
+    cudaGetLastError();
+}
+
+size_t jsmem_bytes(int n, int R, int cs, bool vsm) {
+    const int npairs = (n + (n & 1)) / 2;
+    const size_t x = std::max<size_t>(2 * static_cast<size_t>(cs) * npairs * 3, static_cast<size_t>(cs) * n + 8);
+    return (static_cast<size_t>(n) * R * (vsm ? 2 : 1) + x) * sizeof(double);
+}
+
+JCfg choose(int n) {
+    jinit();
+    const size_t cap = static_cast<size_t>(g_jcap) - 512;
+    JCfg c{1, std::max(n, 1), 1, 16, 0};
+    for (int cs = 1;; cs *= 2) {
+        const int R = std::max(1, (n + cs - 1) / cs);
+        if (R <= kLPP * 16 && jsmem_bytes(n, R, cs, true) <= cap) {
+            c = {cs, R, 1, 0, jsmem_bytes(n, R, cs, true)};
+            break;
+        }
+        if (cs >= g_jmax_cluster) {
+            const int R2 = std::max(1, (n + g_jmax_cluster - 1) / g_jmax_cluster);
+            if (R2 > kLPP * 16 || jsmem_bytes(n, R2, g_jmax_cluster, false) > cap)
+                throw Error(RUTV_ERR_NOTIMPL, "svd_block: block too large for one cluster");
+            c = {g_jmax_cluster, R2, 0, 0, jsmem_bytes(n, R2, g_jmax_cluster, false)};
+            break;
+        }
+    }
+    const int rpl = (c.R + kLPP - 1) / kLPP;
+    c.rpl = rpl <= 2 ? 2 : rpl <= 4 ? 4 : rpl <= 8 ? 8 : 16;
+    return c;
 }
 
 }  // namespace
 
-int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) {
-    // V chunks in global (worst case) + scratch + completion candidate
-    return n * (n + 16) + 16 * std::max<int64_t>(n, 4) + n + 64;
+int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) { return n * n + n + 64; }
+
+void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol,
+               int max_sweeps) {
+    if (count <= 0) return;
+    const JCfg c = choose(nmax);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(count * c.cs));
+    cfg.blockDim = dim3(kJThreads);
+    cfg.dynamicSmemBytes = c.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = c.cs;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    switch (c.rpl) {
+        case 2: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<2>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
+        case 4: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<4>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
+        case 8: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<8>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
+        default: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<16>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
+    }
+    note_launch();
+    complete_kernel<<<count, 256, 0, stream>>>(d_descs);
+    note_launch();
+    RUTV_CHECK_LAUNCH();
 }
 
 void svd_block(cudaStream_t stream, const DView& a, double* u, double* sigma, double* v,
                double* work, int64_t work_elems, double* dev_status, double tol, int max_sweeps) {
     const int n = static_cast<int>(a.rows);
     if (a.rows != a.cols) throw Error(RUTV_ERR_SHAPE, "svd_block expects a square block");
-    if (work_elems < svd_work_elems(n, max_sweeps)) throw Error(RUTV_ERR_INTERNAL, "svd scratch too small");
-    const int cmax = jmax_cluster();
-    int cs = 1;
-    bool vsm = true;
-    for (;;) {
-        const int R = (n + cs - 1) / cs;
-        if (jsmem(n, R, cs, true) <= static_cast<size_t>(kJSmemCap) - 1024) break;
-        if (cs >= cmax) {
-            vsm = false;
-            break;
-        }
-        cs *= 2;
-    }
-    if (n == 0) cs = 1;
-    const int R = std::max(1, (n + cs - 1) / cs);
-    if (!vsm && jsmem(n, R, cs, false) > static_cast<size_t>(kJSmemCap) - 1024)
-        throw Error(RUTV_ERR_NOTIMPL, "svd_block: block too large for one cluster");
-    JParams P;
-    P.A = a.data;
-    P.lda = a.ld;
-    P.n = n;
-    P.N = n + (n & 1);
-    P.R = R;
-    P.npairs = P.N / 2;
-    P.U = u;
-    P.sigma = sigma;
-    P.V = v;
-    P.vglob = vsm ? nullptr : work;
-    P.gscr = work + static_cast<int64_t>(n) * (n + 16);
-    P.tol = tol;
-    P.max_sweeps = max_sweeps;
-    P.status = dev_status;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kJThreads);
-    cfg.dynamicSmemBytes = jsmem(n, R, cs, vsm);
-    cfg.stream = stream;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = cs;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel, P));
-    note_launch();
-    double* cand = P.gscr + 16 * std::max(n, 4);
-    complete_kernel<<<1, 256, 0, stream>>>(u, n, dev_status, cand);
-    note_launch();
-    RUTV_CHECK_LAUNCH();
+    if (work_elems < svd_work_elems(n, max_sweeps) + 16)
+        throw Error(RUTV_ERR_INTERNAL, "svd scratch too small");
+    SvdDesc h{a.data, a.ld, n, 0, u, sigma, v, work, dev_status};
+    // descriptor lives at the end of the work buffer (stream-ordered copy)
+    SvdDesc* dd = reinterpret_cast<SvdDesc*>(work + svd_work_elems(n, max_sweeps));
+    static_assert(sizeof(SvdDesc) <= 16 * sizeof(double), "descriptor slot");
+    RUTV_CUDA(cudaMemcpyAsync(dd, &h, sizeof h, cudaMemcpyHostToDevice, stream));
+    // pageable source: cudaMemcpyAsync stages `h` before returning
+    svd_batch(stream, dd, 1, n, tol, max_sweeps);
 }
 
 }  // namespace rutv

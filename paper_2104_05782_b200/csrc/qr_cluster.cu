@@ -1,0 +1,410 @@
+// hqr.cu -- Householder panel QR on a thread-block cluster (sm_100a DSMEM).
+//
+// Restates hqr_inplace + house (proj/src/householder.cpp:20-67) with the
+// reference's convention, which is NOT LAPACK's and is load-bearing for
+// parity:
+//   sigma = sum(tail^2); sigma == 0 -> (alpha >= 0: beta = alpha, tau = 0)
+//                                      (alpha <  0: beta = -alpha, tau = 2)
+//   else beta = sqrt(alpha^2 + sigma) >= 0,
+//        head = alpha >= 0 ? -sigma/(alpha+beta) : alpha - beta   (Parlett),
+//        v_tail = tail/head, tau = -head/beta.
+//
+// Layout: the s x w panel is split by rows over a cluster of CS CTAs; each CTA
+// keeps its row chunk (all w columns, column-major with an odd leading
+// dimension so column-strided lane accesses are bank-conflict free) resident
+// in shared memory for the whole factorisation.  Per column j:
+//   (A) every CTA's partial [sigma_j, x_j'a_{j+1}, ..., x_j'a_{w-1}]
+//       (x_j = unscaled tail of column j) is reduce-scattered over DSMEM:
+//       entry e goes to CTA e % CS; sigma partials and the head alpha are
+//       all-gathered -- cluster barrier;
+//   (B) house() scalars (warp 0); each owner reduces its entries in rank
+//       order and broadcasts w_k = tau (a(j,k) + d_k / head) -- algebraically
+//       the reference's tau (a(j,k) + sum v_i a(i,k)) -- cluster barrier;
+//   then a row pass scales the reflector (v = x / head, the reference's
+//   division) and updates column j+1, and ONE fused pass over the trailing
+//   columns applies a_k -= w_k v and, in the same sweep, accumulates the NEXT
+//   column's partials x_{j+1}' a_k.  Lanes map to columns and loop over rows
+//   (the reflector value is a shared-memory broadcast): no warp reductions in
+//   the inner loop.  Reductions are in fixed rank order -> deterministic.
+// Panels whose chunk does not fit the cluster's shared memory are factored in
+// column sub-panels, the trailing columns updated with DMMA GEMMs (blocked
+// right-looking, same reflectors).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "rutv_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rutv {
+
+namespace {
+
+constexpr int kQrThreads = 512;
+constexpr int kQrWarps = kQrThreads / 32;
+int kSmemCap = 227 * 1024 - 1024;  // refined at first use (dyn_smem_cap)
+
+struct QrSmem {
+    double* chunk;  // w columns x LD
+    double* ms1;    // [CS][slots] partial dots, reduce-scattered to the entry's owner
+    double* hd1;    // [slots] head-row entries for owned entries (from the row owner)
+    double* sa;     // [CS + 1] sigma partials (all-gathered) + alpha (slot CS)
+    double* wvb;    // [w] broadcast w_k values (index e = k - j)
+    double* red;    // [w] local combine scratch
+    double* part;   // [16][w] per-row-group partials
+    double* hs;     // [4] house scalars: beta, tau, head, scale
+};
+
+__device__ __forceinline__ QrSmem carve(double* sm, int w, int LD, int CS) {
+    const int slots = (w + CS - 1) / CS;
+    QrSmem s;
+    s.chunk = sm;
+    s.ms1 = s.chunk + static_cast<size_t>(w) * LD;
+    s.hd1 = s.ms1 + static_cast<size_t>(CS) * slots;
+    s.sa = s.hd1 + slots;
+    s.wvb = s.sa + CS + 1;
+    s.red = s.wvb + w;
+    s.part = s.red + w;
+    s.hs = s.part + static_cast<size_t>(kQrWarps) * w;
+    return s;
+}
+
+__device__ __forceinline__ int row_groups(int nk) {
+    const int ncg = (nk + 31) >> 5;
+    return ncg >= 16 ? 1 : kQrWarps / ncg;
+}
+
+// Fused pass.  Columns kc in [k0, w) (lanes <-> columns, 32 per column group,
+// warps split into column groups x row groups).  When upd0, columns >= kupd
+// get a -= wv[kc] * v_i on rows [iu, rc) (v = chunk column jv).  Every
+// column's dot with the NEXT column xn (chunk column jn, rows [id, rc),
+// id >= iu) is accumulated into part[rg][kc].
+__device__ __forceinline__ void fused_pass(const QrSmem& S, int LD, int w, int k0, int kupd, int rc,
+                                           bool upd0, int jv, int iu, const double* wv, int jn, int id) {
+    const int nk = w - k0;
+    if (nk <= 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncg = (nk + 31) >> 5;
+    const int nrg = row_groups(nk);
+    const int rg = warp / ncg, cg_ = warp - rg * ncg;
+    if (rg >= nrg) return;
+    const int kc = k0 + cg_ * 32 + lane;
+    if (kc >= w) return;
+    const bool upd = upd0 && kc >= kupd;
+    const int lo = upd0 ? iu : id;
+    const int span = max(0, rc - lo);
+    const int per = (span + nrg - 1) / nrg;
+    const int rb = lo + rg * per, re = min(rc, rb + per);
+    double* col = S.chunk + static_cast<size_t>(kc) * LD;
+    const double* ncol = S.chunk + static_cast<size_t>(jn) * LD;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (upd) {
+        const double* vcol = S.chunk + static_cast<size_t>(jv) * LD;
+        const double wk = wv[kc];
+        int i = rb;
+        const int e1 = min(re, id);
+        for (; i < e1; ++i) col[i] -= wk * vcol[i];  // rows in [iu, id): update only
+        for (; i + 1 < re; i += 2) {
+            const double a0 = col[i] - wk * vcol[i];
+            const double a1 = col[i + 1] - wk * vcol[i + 1];
+            col[i] = a0;
+            col[i + 1] = a1;
+            acc0 += ncol[i] * a0;
+            acc1 += ncol[i + 1] * a1;
+        }
+        if (i < re) {
+            const double a0 = col[i] - wk * vcol[i];
+            col[i] = a0;
+            acc0 += ncol[i] * a0;
+        }
+    } else {
+        int i = max(rb, id);
+        for (; i + 1 < re; i += 2) {
+            acc0 += ncol[i] * col[i];
+            acc1 += ncol[i + 1] * col[i + 1];
+        }
+        if (i < re) acc0 += ncol[i] * col[i];
+    }
+    S.part[static_cast<size_t>(rg) * w + kc] = acc0 + acc1;
+}
+
+__global__ void __launch_bounds__(kQrThreads, 1)
+    hqr_cluster_kernel(double* A, int64_t lda, int s, int w, int p, int R, int LD, int lcs, double* tau) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = 1 << lcs;
+    const int rank = static_cast<int>(cluster.block_rank());
+    extern __shared__ __align__(16) double sm[];
+    const QrSmem S = carve(sm, w, LD, CS);
+    const int slots = (w + CS - 1) >> lcs;
+    const int tid = threadIdx.x;
+    const int r_beg = rank * R;
+    const int rc = max(0, min(s, r_beg + R) - r_beg);  // my row count
+
+    if (rc > 0)
+        for (int idx = tid; idx < w * rc; idx += kQrThreads) {
+            const int c = idx / rc, i = idx - c * rc;
+            S.chunk[static_cast<size_t>(c) * LD + i] = A[(r_beg + i) + static_cast<int64_t>(c) * lda];
+        }
+    if (CS > 1) cluster.sync(); else __syncthreads();  // all CTAs live before any DSMEM traffic
+
+    auto rmt = [&](double* local, int dst) { return CS > 1 ? cluster.map_shared_rank(local, dst) : local; };
+    auto bar = [&]() {
+        if (CS > 1) cluster.sync(); else __syncthreads();
+    };
+
+    // Phase A for column jn: combine row-group partials, reduce-scatter entry
+    // e = k - jn to its owner (e % CS); all-gather the sigma partial; the row
+    // owner ships row jn: alpha to everyone, head entries to their owners.
+    auto phaseA = [&](int jn) {
+        const int nk = w - jn;
+        const int nrg = row_groups(nk);
+        for (int e = tid; e < nk; e += kQrThreads) {
+            double v = 0.0;
+            for (int g = 0; g < nrg; ++g) v += S.part[static_cast<size_t>(g) * w + jn + e];
+            S.red[e] = v;
+        }
+        __syncthreads();
+        const bool owner = jn >= r_beg && jn < r_beg + rc;
+        const double* hrow_src = S.chunk + (jn - r_beg);  // row jn: column c at hrow_src[c*LD]
+        for (int e = tid; e < nk; e += kQrThreads) {
+            const int dst = e & (CS - 1), sl = e >> lcs;
+            rmt(S.ms1, dst)[static_cast<size_t>(rank) * slots + sl] = S.red[e];
+            if (owner) rmt(S.hd1, dst)[sl] = hrow_src[static_cast<size_t>(jn + e) * LD];
+        }
+        if (tid < CS) {
+            double* sa = rmt(S.sa, tid);
+            sa[rank] = S.red[0];
+            if (owner) sa[CS] = hrow_src[static_cast<size_t>(jn) * LD];
+        }
+    };
+
+    if (p > 0) {  // initial partials for column 0 (dots over rows > 0)
+        fused_pass(S, LD, w, 0, w, rc, false, 0, 0, nullptr, 0, max(0, 1 - r_beg));
+        __syncthreads();
+        phaseA(0);
+    }
+
+    for (int j = 0; j < p; ++j) {
+        const int nk = w - j;
+        bar();  // (A) partials of column j visible at their owners
+        if (tid < 32) {  // house() scalars (householder.cpp:20-34), one warp
+            double sigma = 0.0;
+            for (int r = 0; r < CS; ++r) sigma += S.sa[r];
+            const double alpha = S.sa[CS];
+            double beta, tj, head = 1.0, scale = 0.0;
+            if (sigma == 0.0) {
+                if (alpha >= 0.0) {
+                    beta = alpha;
+                    tj = 0.0;
+                } else {
+                    beta = -alpha;
+                    tj = 2.0;
+                }
+            } else {
+                beta = sqrt(alpha * alpha + sigma);
+                head = alpha >= 0.0 ? -sigma / (alpha + beta) : alpha - beta;
+                tj = -head / beta;
+                scale = 1.0;
+            }
+            if (tid == 0) {
+                S.hs[0] = beta;
+                S.hs[1] = tj;
+                S.hs[2] = head;
+                S.hs[3] = scale;
+                if (rank == 0) tau[j] = tj;
+            }
+        }
+        __syncthreads();
+        const double beta = S.hs[0], tj = S.hs[1], head = S.hs[2];
+        const bool scale = S.hs[3] != 0.0;
+        // owned entries: w_k = tau (a(j,k) + d_k / head), broadcast to every CTA
+        for (int sl = tid; (sl << lcs) + rank < nk; sl += kQrThreads) {
+            const int e = (sl << lcs) + rank;
+            if (e == 0) continue;
+            double d = 0.0;
+            for (int r = 0; r < CS; ++r) d += S.ms1[static_cast<size_t>(r) * slots + sl];
+            const double wv = tj * (S.hd1[sl] + (scale ? d / head : d));
+            for (int dst = 0; dst < CS; ++dst) rmt(S.wvb, dst)[e] = wv;
+        }
+        bar();  // (B) w vector visible everywhere
+        // row pass: scale the reflector, update column j+1 (rows > j) and row j
+        const int iu = max(0, j + 1 - r_beg);
+        double* xj = S.chunk + static_cast<size_t>(j) * LD;
+        double* xn = S.chunk + static_cast<size_t>(j + 1) * LD;
+        const double w1 = nk > 1 ? S.wvb[1] : 0.0;
+        const bool upd_next = nk > 1 && tj != 0.0;
+        for (int i = iu + tid; i < rc; i += kQrThreads) {
+            const double v = scale ? xj[i] / head : xj[i];
+            xj[i] = v;
+            if (upd_next) xn[i] -= w1 * v;
+        }
+        const bool owner = j >= r_beg && j < r_beg + rc;
+        if (owner) {
+            const int jl = j - r_beg;
+            if (tid == 0) xj[jl] = beta;
+            if (tj != 0.0)
+                for (int e = 1 + tid; e < nk; e += kQrThreads) S.chunk[static_cast<size_t>(j + e) * LD + jl] -= S.wvb[e];
+        }
+        __syncthreads();
+        if (j + 1 >= w) break;
+        // fused pass: update columns j+2.. and accumulate the next partials
+        // x_{j+1}' a_k over rows > j+1 (k = j+1 gives the next sigma).
+        fused_pass(S, LD, w, j + 1, j + 2, rc, tj != 0.0, j, iu, S.wvb - j, j + 1, max(0, j + 2 - r_beg));
+        __syncthreads();
+        if (j + 1 < p) phaseA(j + 1);
+    }
+
+    if (rc > 0)
+        for (int idx = tid; idx < w * rc; idx += kQrThreads) {
+            const int c = idx / rc, i = idx - c * rc;
+            A[(r_beg + i) + static_cast<int64_t>(c) * lda] = S.chunk[static_cast<size_t>(c) * LD + i];
+        }
+    if (CS > 1) cluster.sync();  // no CTA exits while a peer may still write into it
+}
+
+size_t cluster_smem_bytes(int w, int LD, int cs) {
+    const size_t slots = (static_cast<size_t>(w) + cs - 1) / cs;
+    return (static_cast<size_t>(w) * LD + (static_cast<size_t>(cs) + 1) * slots + cs + 1 +
+            2 * static_cast<size_t>(w) + static_cast<size_t>(kQrWarps) * w + 4) *
+           sizeof(double);
+}
+
+int g_max_cluster = 0;  // largest cluster size the device accepted (probe once)
+
+int max_cluster() {
+    if (g_max_cluster) return g_max_cluster;
+    kSmemCap = dyn_smem_cap(reinterpret_cast<const void*>(hqr_cluster_kernel));
+    RUTV_CUDA(cudaFuncSetAttribute(hqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RUTV_CUDA(cudaFuncSetAttribute(hqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemCap));
+    int best = 8;
+    for (int cs : {16, 8}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kQrThreads);
+        cfg.dynamicSmemBytes = kSmemCap;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = cs;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, hqr_cluster_kernel, &cfg) == cudaSuccess &&
+            nclusters > 0) {
+            best = cs;
+            break;
+        }
+        cudaGetLastError();
+    }
+    g_max_cluster = best;
+    return best;
+}
+
+inline int odd_ld(int64_t R) { return static_cast<int>(R | 1); }
+
+// Largest column count one cluster launch of cs CTAs can hold for s rows.
+int cluster_cols_capacity(int64_t s, int cs) {
+    const int LD = odd_ld((s + cs - 1) / cs);
+    int w = static_cast<int>(std::max<int64_t>(0, (kSmemCap - 512) / (8 * (LD + 2 + kQrWarps))));
+    while (w > 0 && cluster_smem_bytes(w, LD, cs) > static_cast<size_t>(kSmemCap) - 512) --w;
+    return w;
+}
+
+// Cluster size: enough CTAs for the chunk to fit, and roughly one CTA per 192
+// rows (per-column work vs. the DSMEM all-gather, which grows with CS).
+int pick_cluster(int64_t s, int64_t w, int cmax) {
+    int cs = 1;
+    while (cs < cmax && (s + cs - 1) / cs > 192) cs *= 2;
+    while (cs < cmax && cluster_cols_capacity(s, cs) < w) cs *= 2;
+    return cs;
+}
+
+void launch_cluster(cudaStream_t stream, const DView& a, double* tau, int cs) {
+    const int s = static_cast<int>(a.rows), w = static_cast<int>(a.cols);
+    const int p = std::min(s, w);
+    const int R = (s + cs - 1) / cs;
+    const int LD = odd_ld(R);
+    const size_t smem = cluster_smem_bytes(w, LD, cs);
+    if (smem > static_cast<size_t>(kSmemCap)) throw Error(RUTV_ERR_INTERNAL, "hqr: sub-panel exceeds cluster capacity");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kQrThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cs;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int lcs = 0;
+    while ((1 << lcs) < cs) ++lcs;
+    RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_cluster_kernel, a.data, a.ld, s, w, p, R, LD, lcs, tau));
+    note_launch();
+}
+
+}  // namespace
+
+int64_t hqr_work_elems(int64_t s, int64_t w) {
+    // W (s x nb) + Gram (nb x nb) + Tsub (nb x nb) + Z, Z2 (nb x w) + gemm split-K scratch
+    const int64_t nb = std::min<int64_t>(w, 512);
+    return s * nb + 2 * nb * nb + 2 * nb * w + gemm_work_elems(nb, w, s) +
+           gemm_work_elems(nb, nb, s) + 1024;
+}
+
+void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, int64_t ldt,
+               double* scratch, int64_t scratch_elems) {
+    const int64_t s = a.rows, w = a.cols, p = std::min(s, w);
+    if (p == 0) return;
+    const int cmax = max_cluster();
+    const int cap = cluster_cols_capacity(s, cmax);
+    if (cap < 1) throw Error(RUTV_ERR_NOTIMPL, "hqr: panel too tall for one cluster");
+    if (cap >= w && w <= 512) {
+        launch_cluster(stream, a, tau, pick_cluster(s, w, cmax));
+    } else {
+        // Blocked right-looking: sub-panels of nb columns, trailing update
+        // A_trail <- (I - W T W')' A_trail = A_trail - W T' (W' A_trail).
+        const int64_t nb = std::min<int64_t>(512, std::max<int64_t>(1, (cap / 8) * 8 > 0 ? (cap / 8) * 8 : cap));
+        double* W = scratch;
+        double* Gm = W + s * nb;
+        double* Ts = Gm + nb * nb;
+        double* Z = Ts + nb * nb;
+        double* Z2 = Z + nb * w;
+        double* gw = Z2 + nb * w;
+        const int64_t gw_elems = scratch_elems - (gw - scratch);
+        for (int64_t j0 = 0; j0 < p; j0 += nb) {
+            const int64_t jb = std::min(nb, p - j0);
+            DView sub = a.block(j0, j0, s - j0, jb);
+            launch_cluster(stream, sub, tau + j0, pick_cluster(s - j0, jb, cmax));
+            const int64_t rest = w - j0 - jb;
+            if (rest <= 0) continue;
+            DView trail = a.block(j0, j0 + jb, s - j0, rest);
+            DView Wv(s - j0, jb, s - j0, W);
+            make_w(stream, sub, jb, Wv);
+            DView Gv(jb, jb, jb, Gm), Tv(jb, jb, jb, Ts);
+            gemm(stream, 1.0, Op::T, Wv, Op::N, Wv, 0.0, Gv, gw, gw_elems);
+            form_t(stream, Gm, jb, tau + j0, jb, Ts, jb);
+            DView Zv(jb, rest, jb, Z), Z2v(jb, rest, jb, Z2);
+            gemm(stream, 1.0, Op::T, Wv, Op::N, trail, 0.0, Zv, gw, gw_elems);
+            gemm(stream, 1.0, Op::T, Tv, Op::N, Zv, 0.0, Z2v, gw, gw_elems);
+            gemm(stream, -1.0, Op::N, Wv, Op::N, Z2v, 1.0, trail, gw, gw_elems);
+        }
+    }
+    if (twy) {
+        // Twy of the whole panel: Gram of W then the forward recurrence.
+        if (scratch_elems < s * p + p * p) throw Error(RUTV_ERR_INTERNAL, "hqr: scratch too small");
+        double* W = scratch;
+        double* Gm = W + s * p;
+        double* gw = Gm + p * p;
+        DView Wv(s, p, s, W), Gv(p, p, p, Gm);
+        make_w(stream, a, p, Wv);
+        gemm(stream, 1.0, Op::T, Wv, Op::N, Wv, 0.0, Gv, gw, scratch_elems - (gw - scratch));
+        form_t(stream, Gm, p, tau, p, twy, ldt);
+    }
+}
+
+}  // namespace rutv

@@ -15,18 +15,31 @@
 //
 // HBM layout: V (n x n) and T (n x n) are stacked in ONE column-major buffer
 // VT of (n + n) rows, V on top (rows 0..n) and T below (rows n..2n), so the
-// V-side transform of step i is a single pair of GEMMs over rows
-// [0, 2n) x columns [r0, n): the reference's three apply_q_right calls on
-// T22, T(0:r0, r0:) and V(:, r0:) collapse into one, and the rows that are
-// off the critical path (V and the finished T rows) are the contiguous
-// prefix [0, n + r0).  Block reflectors are applied in the form
+// V-side transform of step i is over rows [0, 2n) x columns [r0, n): the
+// reference's three apply_q_right calls on T22, T(0:r0, r0:) and V(:, r0:)
+// become the critical rows [n + r0, 2n) (T22) plus ONE off-critical block,
+// the contiguous prefix [0, n + r0) (V and the finished T rows).  Block
+// reflectors are applied as
 //   B Q = B - (B W) M',   Q' B = B - M (W' B),   M = W Twy'
-// (M formed once per step, shared by every target), which is the
-// reference's three-GEMM apply with the small Twy product re-associated.
+// (M formed once per step, shared by every target) -- the reference's
+// three-GEMM apply with the small Twy product re-associated.
+//
+// Schedule.  Stream A (the caller's) carries the critical chain, the only
+// work the NEXT step's trailing matrix depends on:
+//   sketch -> QR(Y) -> V-apply on T22 -> QR(panel) -> Qu' on T22(:, b:).
+// Stream B carries the V/U accumulation of the step.  The beta stage is
+// DEFERRED: beta_stage only ever left-multiplies finished ROW blocks
+// (strip T(r0:r0+b, r0+b:) by Us') and right-multiplies finished COLUMN
+// blocks (T(0:r0, r0:r0+b), U(:, r0:r0+b), V(:, r0:r0+b) by Vs / Us) and
+// writes the finished panel columns; later steps only right-multiply columns
+// >= r0+b.  Left and right multiplications commute, so every step's R is
+// saved and all SVDs run as ONE batched launch after the loop, followed by
+// the strips (disjoint row blocks) and the right-multiplies (disjoint column
+// blocks).  Mathematically identical to the reference order; the rounding
+// differs only at the ulp level.  Results are bit-identical with overlap off.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -57,12 +70,6 @@ struct DevBuf {
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
-    DevBuf& operator=(DevBuf&& o) noexcept {
-        std::swap(p, o.p);
-        std::swap(st, o.st);
-        return *this;
-    }
     ~DevBuf() {
         if (p) cudaFreeAsync(p, st);
     }
@@ -82,7 +89,6 @@ void configure_pool(int device) {
 struct Profiler {
     bool on = false;
     cudaStream_t st;
-    std::vector<std::string> names;
     std::vector<double> ms;
     std::vector<cudaEvent_t> evs;
     std::vector<int> ev_phase;
@@ -94,21 +100,20 @@ struct Profiler {
         evs.push_back(e);
         ev_phase.push_back(phase);
     }
-    void finish() {
+    void finish(int nphase) {
         if (!on) return;
         cudaEventSynchronize(evs.back());
-        ms.assign(names.size(), 0.0);
+        ms.assign(static_cast<size_t>(nphase), 0.0);
         for (size_t i = 1; i < evs.size(); ++i) {
             float t = 0.f;
             cudaEventElapsedTime(&t, evs[i - 1], evs[i]);
-            ms[ev_phase[i]] += t;
+            ms[static_cast<size_t>(ev_phase[i])] += t;
         }
         for (auto e : evs) cudaEventDestroy(e);
         evs.clear();
     }
 };
 
-thread_local std::vector<std::string> t_prof_names;
 thread_local std::vector<double> t_prof_ms;
 
 enum Phase { P_START, P_SKETCH, P_QRV, P_APPLYV, P_QRU, P_APPLYU, P_SVD, P_BETA, P_FINAL, P_N };
@@ -117,24 +122,64 @@ const char* kPhaseNames[P_N] = {"start", "sketch", "qr_v", "apply_v", "qr_u", "a
 
 }  // namespace
 
-
-// Factorizes a square n x n device matrix; results written to the device
-// output views.  Throws rutv::Error.
 void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& fa) {
     const int64_t b = fa.b;
     configure_pool(device);
     Profiler prof;
     prof.on = std::getenv("RUTV_PROFILE") && std::strcmp(std::getenv("RUTV_PROFILE"), "0") != 0;
     prof.st = st;
-    for (int i = 0; i < P_N; ++i) prof.names.push_back(kPhaseNames[i]);
     prof.mark(P_START);
     gemm_profile_begin();
+    const char* ov_env = std::getenv("RUTV_OVERLAP");
+    const bool overlap = fa.overlap && !prof.on && !(ov_env && std::strcmp(ov_env, "0") == 0);
 
     const bool bu = fa.build_u, bv = fa.build_v;
-    const int64_t vr = bv ? n : 0;          // V rows on top of T in VT
+    const int64_t vr = bv ? n : 0;  // V rows on top of T in VT
     const int64_t ldvt = rup(std::max<int64_t>(vr + n, 1), 4);
     const int64_t ldu = rup(std::max<int64_t>(n, 1), 4);
     const int64_t bb = std::min(b, std::max<int64_t>(n, 1));
+
+    // ---- step plan: r0, s and kind of every loop iteration (max_steps honoured)
+    struct StepInfo {
+        int64_t r0, s;
+        bool tail;
+    };
+    std::vector<StepInfo> plan;
+    for (int64_t i = 0;; ++i) {
+        const int64_t r0 = i * b, s = n - r0;
+        if (s <= 0) break;
+        if (fa.max_steps >= 0 && static_cast<int>(plan.size()) >= fa.max_steps) break;
+        plan.push_back({r0, s, s <= b});
+        if (s <= b) break;
+    }
+    const int nsteps = static_cast<int>(plan.size());
+
+    cudaStream_t sB = st;
+    if (overlap) RUTV_CUDA(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        bool own;
+        ~StreamGuard() {
+            if (own) cudaStreamDestroy(s);
+        }
+    } sguard{sB, overlap};
+    std::vector<cudaEvent_t> events;
+    struct EventGuard {
+        std::vector<cudaEvent_t>& ev;
+        ~EventGuard() {
+            for (auto e : ev) cudaEventDestroy(e);
+        }
+    } eguard{events};
+    auto record = [&](cudaStream_t s) {
+        cudaEvent_t e;
+        RUTV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        RUTV_CUDA(cudaEventRecord(e, s));
+        events.push_back(e);
+        return e;
+    };
+    auto wait = [&](cudaStream_t s, cudaEvent_t e) {
+        if (overlap && e) RUTV_CUDA(cudaStreamWaitEvent(s, e, 0));
+    };
 
     DevBuf VT(ldvt * std::max<int64_t>(n, 1), st);
     DevBuf U(bu ? ldu * n : 1, st);
@@ -148,137 +193,192 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
     if (bv) set_identity(st, vt.block(0, 0, n, n));
 
     const int64_t sb = std::max<int64_t>(n * bb, 1);
-    DevBuf G(fa.dG ? 1 : sb, st), Y(sb, st), Z(sb, st), Wv(sb, st), Mv(sb, st), Wu(sb, st), Mu(sb, st);
-    DevBuf Zx(std::max<int64_t>((vr + n) * bb, 1), st);  // B*W for all VT rows / U rows
-    DevBuf Zl(std::max<int64_t>(bb * n, 1), st);         // W'*B from the left, strip temp
-    DevBuf Twy(bb * bb, st), Gram(bb * bb, st), tau(bb + 1, st);
-    DevBuf Rb(bb * bb, st), Us(bb * bb, st), Vs(bb * bb, st), sig(bb + 1, st);
-    const int64_t nsteps_max = n / std::max<int64_t>(b, 1) + 2;
-    DevBuf jstat(4 * nsteps_max, st);
-    RUTV_CUDA(cudaMemsetAsync(jstat.p, 0, static_cast<size_t>(4 * nsteps_max) * 8, st));
+    // stream A private
+    DevBuf G(fa.dG ? 1 : sb, st), Y(sb, st), Z(sb, st), ZxA(std::max<int64_t>((vr + n) * bb, 1), st);
+    DevBuf ZlA(sb, st), Twy(bb * bb, st), Gram(bb * bb, st), tau(bb + 1, st);
+    // double-buffered A -> B hand-off
+    DevBuf Wv0(sb, st), Wv1(sb, st), Mv0(sb, st), Mv1(sb, st);
+    DevBuf Wu0(sb, st), Wu1(sb, st), Mu0(sb, st), Mu1(sb, st);
+    double* Wv[2] = {Wv0.p, Wv1.p};
+    double* Mv[2] = {Mv0.p, Mv1.p};
+    double* Wu[2] = {Wu0.p, Wu1.p};
+    double* Mu[2] = {Mu0.p, Mu1.p};
+    // stream B private
+    DevBuf ZxB(std::max<int64_t>((vr + n) * bb, 1), st);
+    // deferred beta stage: every step's R, Us, Vs, sigma, status, scratch
+    const int ns = std::max(nsteps, 1);
     const int64_t svdw = svd_work_elems(bb, 30);
-    DevBuf SvdW(svdw, st);
-    int64_t gw_elems = std::max<int64_t>({gemm_work_elems(n, bb, n), gemm_work_elems(bb, n, n),
-                                          gemm_work_elems(vr + n, bb, n), gemm_work_elems(bb, bb, n),
-                                          gemm_work_elems(bb, n, bb), 1});
-    DevBuf GW(gw_elems, st);
+    DevBuf Rall(ns * bb * bb, st), Usall(ns * bb * bb, st), Vsall(ns * bb * bb, st);
+    DevBuf Sall(ns * (bb + 1), st), Jst(ns * 4, st), SvdW(ns * svdw, st);
+    const int64_t desc_words = (static_cast<int64_t>(sizeof(SvdDesc)) * ns + 7) / 8;
+    DevBuf Ddesc(desc_words, st);
+    RUTV_CUDA(cudaMemsetAsync(Jst.p, 0, static_cast<size_t>(ns) * 32, st));
+    const int64_t gw_elems =
+        std::max<int64_t>({gemm_work_elems(n, bb, n), gemm_work_elems(bb, n, n), gemm_work_elems(vr + n, bb, n),
+                           gemm_work_elems(bb, bb, n), gemm_work_elems(bb, n, bb), gemm_work_elems(vr + n, bb, bb),
+                           1});
+    DevBuf GWA(gw_elems, st), GWB(gw_elems, st);
     const int64_t hqw = hqr_work_elems(n, bb);
     DevBuf HQ(hqw, st);
+    // allocations are stream-ordered on st; stream B must see them
+    wait(sB, record(st));
+    // declared after every buffer -> destroyed first: stream B drains before any
+    // buffer is released (also on the exception path)
+    struct JoinGuard {
+        cudaStream_t s;
+        bool own;
+        ~JoinGuard() {
+            if (own) cudaStreamSynchronize(s);
+        }
+    } jguard{sB, overlap};
 
-    auto gemm_ = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
-                     const DView& c) { gemm(st, alpha, ta, a, tb, bm, beta, c, GW.p, gw_elems); };
+    auto gemmA = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
+                     const DView& c) { gemm(st, alpha, ta, a, tb, bm, beta, c, GWA.p, gw_elems); };
+    auto gemmB = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
+                     const DView& c) { gemm(sB, alpha, ta, a, tb, bm, beta, c, GWB.p, gw_elems); };
 
-    // Compact-WY pieces of a packed panel qr (s x p): W, Twy, M = W Twy'.
+    // Compact-WY pieces of a packed panel qr (s x p) on stream A: W, Twy, M = W Twy'.
     auto form_wy = [&](const DView& qr, int64_t p, double* wbuf, double* mbuf) {
         const int64_t s = qr.rows;
         DView W(s, p, s, wbuf), M(s, p, s, mbuf);
         make_w(st, qr, p, W);
-        gemm_(1.0, Op::T, W, Op::N, W, 0.0, DView(p, p, p, Gram.p));
+        gemmA(1.0, Op::T, W, Op::N, W, 0.0, DView(p, p, p, Gram.p));
         form_t(st, Gram.p, p, tau.p, p, Twy.p, p);
-        gemm_(1.0, Op::N, W, Op::T, DView(p, p, p, Twy.p), 0.0, M);
+        gemmA(1.0, Op::N, W, Op::T, DView(p, p, p, Twy.p), 0.0, M);
     };
 
     uint64_t pos = 0;  // stream position P_i
-    int steps = 0;
-    int jcount = 0;
-    for (int64_t i = 0;; ++i) {
-        const int64_t r0 = i * b, s = n - r0;
-        if (s <= 0) break;
-        if (fa.max_steps >= 0 && steps >= fa.max_steps) break;
-        ++steps;
+    std::vector<cudaEvent_t> evB;
+    for (int i = 0; i < nsteps; ++i) {
+        const int64_t r0 = plan[static_cast<size_t>(i)].r0, s = plan[static_cast<size_t>(i)].s;
         DView t22 = tmat.block(r0, r0, s, s);
-
-        if (s <= b) {  // ragged tail: one dense SVD (randutv_blocked.cpp:129-137)
-            prof.mark(P_BETA);
-            DView Xin(s, s, s, Rb.p);
-            copy_view(st, Xin, t22);
-            svd_block(st, Xin, Us.p, sig.p, Vs.p, SvdW.p, svdw, jstat.p + 4 * jcount++, 1e-15, 30);
-            prof.mark(P_SVD);
-            write_rect_diag(st, t22, sig.p, s);
-            DView VsV(s, s, s, Vs.p), UsV(s, s, s, Us.p);
-            if (vr + r0 > 0) {
-                DView X = vt.block(0, r0, vr + r0, s);
-                DView tmp(vr + r0, s, vr + r0, Zx.p);
-                gemm_(1.0, Op::N, X, Op::N, VsV, 0.0, tmp);
-                copy_view(st, X, tmp);
-            }
-            if (bu) {
-                DView X = umat.block(0, r0, n, s);
-                DView tmp(n, s, n, Zx.p);
-                gemm_(1.0, Op::N, X, Op::N, UsV, 0.0, tmp);
-                copy_view(st, X, tmp);
-            }
-            prof.mark(P_BETA);
+        double* Ri = Rall.p + static_cast<int64_t>(i) * bb * bb;
+        if (plan[static_cast<size_t>(i)].tail) {  // ragged tail: dense s x s block (:129-137)
+            copy_view(st, DView(s, s, s, Ri), t22);
             break;
         }
+        const int par = i & 1;
+        if (i >= 2) wait(st, evB[static_cast<size_t>(i - 2)]);  // slot `par` free again
 
         // ---- sketch (build_v_alpha, randutv_blocked.cpp:41-50)
         DView Gv(s, b, s, fa.dG ? const_cast<double*>(fa.dG) + pos : G.p);
         if (!fa.dG) normal_fill(st, fa.seed, pos, Gv);
         pos += static_cast<uint64_t>(s * b);
         DView Yv(s, b, s, Y.p), Zv(s, b, s, Z.p);
-        gemm_(1.0, Op::T, t22, Op::N, Gv, 0.0, Yv);
+        gemmA(1.0, Op::T, t22, Op::N, Gv, 0.0, Yv);
         for (int it = 0; it < fa.q; ++it) {
-            gemm_(1.0, Op::N, t22, Op::N, Yv, 0.0, Zv);
-            gemm_(1.0, Op::T, t22, Op::N, Zv, 0.0, Yv);
+            gemmA(1.0, Op::N, t22, Op::N, Yv, 0.0, Zv);
+            gemmA(1.0, Op::T, t22, Op::N, Zv, 0.0, Yv);
         }
         prof.mark(P_SKETCH);
         // ---- V-side QR (:52-53)
         hqr_panel(st, Yv, tau.p, nullptr, 0, HQ.p, hqw);
-        form_wy(Yv, b, Wv.p, Mv.p);
+        form_wy(Yv, b, Wv[par], Mv[par]);
+        const cudaEvent_t evV = record(st);
         prof.mark(P_QRV);
-        // ---- V-apply on all VT rows, columns r0.. (:140-143)
-        {
-            DView X = vt.block(0, r0, vr + n, s);
-            DView ZxV(vr + n, b, vr + n, Zx.p);
-            gemm_(1.0, Op::N, X, Op::N, DView(s, b, s, Wv.p), 0.0, ZxV);
-            gemm_(-1.0, Op::N, ZxV, Op::T, DView(s, b, s, Mv.p), 1.0, X);
+        DView WvV(s, b, s, Wv[par]), MvV(s, b, s, Mv[par]);
+        {  // V-apply, critical rows: T22 (:140)
+            DView X = vt.block(vr + r0, r0, s, s);
+            DView Zx(s, b, s, ZxA.p);
+            gemmA(1.0, Op::N, X, Op::N, WvV, 0.0, Zx);
+            gemmA(-1.0, Op::N, Zx, Op::T, MvV, 1.0, X);
         }
         prof.mark(P_APPLYV);
         // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
         DView panel = t22.block(0, 0, s, b);
         hqr_panel(st, panel, tau.p, nullptr, 0, HQ.p, hqw);
-        form_wy(panel, b, Wu.p, Mu.p);
+        form_wy(panel, b, Wu[par], Mu[par]);
+        copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
         prof.mark(P_QRU);
-        // ---- Q_u' on T22(:, b:) (:147) and U accumulate (:148)
-        {
+        DView WuV(s, b, s, Wu[par]), MuV(s, b, s, Mu[par]);
+        {  // Q_u' on T22(:, b:) (:147)
             DView B = t22.block(0, b, s, s - b);
-            DView Zlv(b, s - b, b, Zl.p);
-            gemm_(1.0, Op::T, DView(s, b, s, Wu.p), Op::N, B, 0.0, Zlv);
-            gemm_(-1.0, Op::N, DView(s, b, s, Mu.p), Op::N, Zlv, 1.0, B);
-            if (bu) {
-                DView X = umat.block(0, r0, n, s);
-                DView ZxU(n, b, n, Zx.p);
-                gemm_(1.0, Op::N, X, Op::N, DView(s, b, s, Wu.p), 0.0, ZxU);
-                gemm_(-1.0, Op::N, ZxU, Op::T, DView(s, b, s, Mu.p), 1.0, X);
+            DView Zl(b, s - b, b, ZlA.p);
+            gemmA(1.0, Op::T, WuV, Op::N, B, 0.0, Zl);
+            gemmA(-1.0, Op::N, MuV, Op::N, Zl, 1.0, B);
+        }
+        const cudaEvent_t evU = record(st);
+        prof.mark(P_APPLYU);
+
+        // ======== stream B: V / U accumulation of step i ========
+        wait(sB, evV);
+        if (vr + r0 > 0) {  // V-apply on V and T(0:r0, r0:) (:141-143)
+            DView X = vt.block(0, r0, vr + r0, s);
+            DView Zx(vr + r0, b, vr + r0, ZxB.p);
+            gemmB(1.0, Op::N, X, Op::N, WvV, 0.0, Zx);
+            gemmB(-1.0, Op::N, Zx, Op::T, MvV, 1.0, X);
+        }
+        wait(sB, evU);
+        if (bu) {  // U accumulate (:148)
+            DView X = umat.block(0, r0, n, s);
+            DView Zx(n, b, n, ZxB.p);
+            gemmB(1.0, Op::N, X, Op::N, WuV, 0.0, Zx);
+            gemmB(-1.0, Op::N, Zx, Op::T, MuV, 1.0, X);
+        }
+        evB.push_back(record(sB));
+        prof.mark(P_APPLYU);
+    }
+    if (overlap) wait(st, record(sB));  // join
+
+    // ======== deferred beta stage (:66-82, :129-137, :150-154) ========
+    if (nsteps > 0) {
+        std::vector<SvdDesc> descs(static_cast<size_t>(nsteps));
+        int64_t nmax = 0;
+        for (int i = 0; i < nsteps; ++i) {
+            const StepInfo& si = plan[static_cast<size_t>(i)];
+            const int64_t w = si.tail ? si.s : b;
+            nmax = std::max(nmax, w);
+            const int64_t off = static_cast<int64_t>(i) * bb * bb;
+            descs[static_cast<size_t>(i)] =
+                SvdDesc{Rall.p + off, w, static_cast<int>(w), 0, Usall.p + off,
+                        Sall.p + static_cast<int64_t>(i) * (bb + 1), Vsall.p + off,
+                        SvdW.p + static_cast<int64_t>(i) * svdw, Jst.p + 4 * i};
+        }
+        RUTV_CUDA(cudaMemcpyAsync(Ddesc.p, descs.data(), sizeof(SvdDesc) * descs.size(),
+                                  cudaMemcpyHostToDevice, st));
+        svd_batch(st, reinterpret_cast<const SvdDesc*>(Ddesc.p), nsteps, static_cast<int>(nmax), 1e-15, 30);
+        prof.mark(P_SVD);
+        const cudaEvent_t evS = record(st);
+        // U right-multiplies on stream B (disjoint buffer)
+        if (bu) {
+            wait(sB, evS);
+            for (int i = 0; i < nsteps; ++i) {
+                const StepInfo& si = plan[static_cast<size_t>(i)];
+                const int64_t w = si.tail ? si.s : b;
+                const int64_t off = static_cast<int64_t>(i) * bb * bb;
+                DView X = umat.block(0, si.r0, n, w);
+                DView tmp(n, w, n, ZxB.p);
+                gemmB(1.0, Op::N, X, Op::N, DView(w, w, w, Usall.p + off), 0.0, tmp);
+                copy_view(sB, X, tmp);
             }
         }
-        prof.mark(P_APPLYU);
-        // ---- beta_stage (:66-82) and the small right-multiplies (:152-154)
-        DView Rv(b, b, b, Rb.p);
-        copy_upper(st, Rv, t22.block(0, 0, b, b));
-        svd_block(st, Rv, Us.p, sig.p, Vs.p, SvdW.p, svdw, jstat.p + 4 * jcount++, 1e-15, 30);
-        prof.mark(P_SVD);
-        write_rect_diag(st, panel, sig.p, b);
-        DView VsV(b, b, b, Vs.p), UsV(b, b, b, Us.p);
-        {
-            DView strip = t22.block(0, b, b, s - b);
-            DView tmp(b, s - b, b, Zl.p);
-            gemm_(1.0, Op::T, UsV, Op::N, strip, 0.0, tmp);
+        // diagonal writes (finished panel columns), then strips (row blocks),
+        // then V/T right-multiplies (column blocks) on stream A
+        for (int i = 0; i < nsteps; ++i) {
+            const StepInfo& si = plan[static_cast<size_t>(i)];
+            const int64_t w = si.tail ? si.s : b;
+            write_rect_diag(st, tmat.block(si.r0, si.r0, si.s, w), Sall.p + static_cast<int64_t>(i) * (bb + 1), w);
+        }
+        for (int i = 0; i < nsteps; ++i) {
+            const StepInfo& si = plan[static_cast<size_t>(i)];
+            if (si.tail) continue;
+            const int64_t off = static_cast<int64_t>(i) * bb * bb;
+            DView strip = tmat.block(si.r0, si.r0 + b, b, si.s - b);
+            DView tmp(b, si.s - b, b, ZlA.p);
+            gemmA(1.0, Op::T, DView(b, b, b, Usall.p + off), Op::N, strip, 0.0, tmp);
             copy_view(st, strip, tmp);
         }
-        if (vr + r0 > 0) {
-            DView X = vt.block(0, r0, vr + r0, b);
-            DView tmp(vr + r0, b, vr + r0, Zx.p);
-            gemm_(1.0, Op::N, X, Op::N, VsV, 0.0, tmp);
+        for (int i = 0; i < nsteps; ++i) {
+            const StepInfo& si = plan[static_cast<size_t>(i)];
+            const int64_t w = si.tail ? si.s : b;
+            if (vr + si.r0 == 0) continue;
+            const int64_t off = static_cast<int64_t>(i) * bb * bb;
+            DView X = vt.block(0, si.r0, vr + si.r0, w);
+            DView tmp(vr + si.r0, w, vr + si.r0, ZxA.p);
+            gemmA(1.0, Op::N, X, Op::N, DView(w, w, w, Vsall.p + off), 0.0, tmp);
             copy_view(st, X, tmp);
         }
-        if (bu) {
-            DView X = umat.block(0, r0, n, b);
-            DView tmp(n, b, n, Zx.p);
-            gemm_(1.0, Op::N, X, Op::N, UsV, 0.0, tmp);
-            copy_view(st, X, tmp);
-        }
+        if (bu && overlap) wait(st, record(sB));
         prof.mark(P_BETA);
     }
 
@@ -288,22 +388,20 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
     if (bv && fa.dV) copy_view(st, DView(n, n, fa.ldv, fa.dV), vt.block(0, 0, n, n));
     prof.mark(P_FINAL);
 
-    // Jacobi statuses: ConvergenceError surfaces like the reference's exception.
-    std::vector<double> hs(static_cast<size_t>(4 * std::max(jcount, 1)));
-    if (jcount > 0)
-        RUTV_CUDA(cudaMemcpyAsync(hs.data(), jstat.p, static_cast<size_t>(4 * jcount) * 8,
+    // Jacobi statuses: ConvergenceError surfaces like the reference's exception
+    // (the first failing step in step order, as the reference would throw).
+    std::vector<double> hs(static_cast<size_t>(4 * ns), 0.0);
+    if (nsteps > 0)
+        RUTV_CUDA(cudaMemcpyAsync(hs.data(), Jst.p, static_cast<size_t>(4 * nsteps) * 8,
                                   cudaMemcpyDeviceToHost, st));
     RUTV_CUDA(cudaStreamSynchronize(st));
-    prof.finish();
+    prof.finish(P_N);
     gemm_profile_end();
-    if (prof.on) {
-        t_prof_names = prof.names;
-        t_prof_ms = prof.ms;
-    }
-    for (int k = 0; k < jcount; ++k)
-        if (hs[4 * k] == RUTV_ERR_CONVERGENCE)
-            throw Error(RUTV_ERR_CONVERGENCE,
-                        "jacobi sweeps exhausted after 30 sweeps", hs[4 * k + 1]);
+    if (prof.on) t_prof_ms = prof.ms;
+    for (int k = 0; k < nsteps; ++k)
+        if (hs[static_cast<size_t>(4 * k)] == RUTV_ERR_CONVERGENCE)
+            throw Error(RUTV_ERR_CONVERGENCE, "jacobi sweeps exhausted after 30 sweeps",
+                        hs[static_cast<size_t>(4 * k + 1)]);
 }
 
 int last_profile(const char** names, double* ms, int cap) {

@@ -108,11 +108,28 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
             double* t, int64_t ldt);
 
 // One-sided Jacobi SVD of a square block (jacobi_svd.cpp:39-148).  Writes U, sigma, V
-// (n x n, ld n).  Status (code, residual) is written to dev_status[0..1] on the
-// device; the caller checks it after synchronising.
+// (n x n, ld n).  Status (code, residual, kept, sweeps) is written to
+// dev_status[0..3] on the device; the caller checks it after synchronising.
 void svd_block(cudaStream_t stream, const DView& a, double* u, double* sigma, double* v,
                double* work, int64_t work_elems, double* dev_status, double tol, int max_sweeps);
+// per-problem scratch (V spill + completion candidate); svd_block needs +16 more
 int64_t svd_work_elems(int64_t n, int max_sweeps);
+
+// One problem of a batched SVD launch (device-resident array of these).
+struct SvdDesc {
+    const double* A;
+    int64_t lda;
+    int n;
+    int pad;
+    double* U;       // n x n, ld n
+    double* sigma;   // n
+    double* V;       // n x n, ld n
+    double* work;    // svd_work_elems(n) doubles
+    double* status;  // 4 doubles: code, residual, kept, sweeps
+};
+// All problems in one launch (one CTA cluster each); nmax = max n.
+void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol,
+               int max_sweeps);
 
 // Leading ncols columns of Q = H_1...H_p from packed qr (householder.cpp:155-173).
 void form_q(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
@@ -139,6 +156,7 @@ struct FactorArgs {
     int64_t ldu;
     double* dV;        // may be null when !build_v
     int64_t ldv;
+    bool overlap = true;  // second stream for the off-critical-path work
 };
 void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& fa);
 int last_profile(const char** names, double* ms, int cap);

@@ -104,3 +104,17 @@ def test_config1_shape_invariants(kind):
     sa = np.linalg.svd(a, compute_uv=False)
     st = np.linalg.svd(t, compute_uv=False)
     assert np.max(np.abs(sa - st)) < 1e-11 * sa[0]
+
+
+def test_overlap_is_bit_identical():
+    """Two-stream schedule == single-stream schedule, bit for bit."""
+    import os
+    a = oracle.gaussian_matrix(700, 700, 77)
+    r1 = rutv.factorize(a, b=64, q=1, seed=3)
+    os.environ["RUTV_OVERLAP"] = "0"
+    try:
+        r2 = rutv.factorize(a, b=64, q=1, seed=3)
+    finally:
+        os.environ.pop("RUTV_OVERLAP")
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
