@@ -144,7 +144,7 @@ struct SmemGeom {
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, bool VEC>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
     dgemm_kernel(const GemmParams p) {
     constexpr int NWM = BM / WM, NWN = BN / WN, NT = NWM * NWN * 32;
     constexpr int MI = WM / 16, NI = WN / 8;
@@ -262,6 +262,23 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 #pragma unroll
             for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
 
+    // beta != 0: prefetch this thread's C fragment now so the epilogue's
+    // read-modify-write does not serialise on global-load latency (the
+    // rank-b updates have K = b, a mainloop of only a few k-tiles).
+    const bool direct = p.splits == 1;
+    const bool use_c = direct && p.beta != 0.0;
+    double cpre[MI][NI][4];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t m = m0 + wm * WM + mi * 16 + g + (r >= 2 ? 8 : 0);
+                const int64_t n = n0 + wn * WN + ni * 8 + 2 * t + (r & 1);
+                cpre[mi][ni][r] = (use_c && m < M && n < N) ? __ldg(p.C + m + n * p.ldc) : 0.0;
+            }
+
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
         if (s < KT) load_tile(s, kbeg + static_cast<int64_t>(s) * BK);
@@ -298,7 +315,6 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     }
     cp_async_wait<0>();
 
-    const bool direct = p.splits == 1;
     double* wbase = p.work + static_cast<int64_t>(blockIdx.z) * M * N;
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
@@ -310,10 +326,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 const int64_t n = n0 + wn * WN + ni * 8 + 2 * t + (r & 1);
                 if (m < M && n < N) {
                     if (direct) {
-                        double* cp = p.C + m + n * p.ldc;
                         double v = p.alpha * acc[mi][ni][r];
-                        if (p.beta != 0.0) v += p.beta * *cp;
-                        *cp = v;
+                        if (use_c) v += p.beta * cpre[mi][ni][r];
+                        p.C[m + n * p.ldc] = v;
                     } else {
                         wbase[m + n * M] = acc[mi][ni][r];
                     }

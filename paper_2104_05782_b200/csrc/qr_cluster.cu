@@ -13,14 +13,14 @@
 // keeps its row chunk (all w columns, column-major with an odd leading
 // dimension so column-strided lane accesses are bank-conflict free) resident
 // in shared memory for the whole factorisation.  Per column j:
-//   (A) every CTA's partial [sigma_j, x_j'a_{j+1}, ..., x_j'a_{w-1}]
-//       (x_j = unscaled tail of column j) is reduce-scattered over DSMEM:
-//       entry e goes to CTA e % CS; sigma partials and the head alpha are
-//       all-gathered -- cluster barrier;
-//   (B) house() scalars (warp 0); each owner reduces its entries in rank
-//       order and broadcasts w_k = tau (a(j,k) + d_k / head) -- algebraically
-//       the reference's tau (a(j,k) + sum v_i a(i,k)) -- cluster barrier;
-//   then a row pass scales the reflector (v = x / head, the reference's
+//   every CTA's partial [sigma_j, x_j'a_{j+1}, ..., x_j'a_{w-1}]
+//   (x_j = unscaled tail of column j) and the row owner's row j are
+//   all-gathered with st.async remote stores that complete on each
+//   receiver's mbarrier (transaction bytes) -- no cluster barrier, no
+//   fences, one DSMEM hop per column; every CTA reduces in rank order
+//   (identical results everywhere), warp 0 computes house(), and
+//   w_k = tau (a(j,k) + d_k / head) -- algebraically the reference's
+//   tau (a(j,k) + sum v_i a(i,k)).  Then a row pass scales the reflector (v = x / head, the reference's
 //   division) and updates column j+1, and ONE fused pass over the trailing
 //   columns applies a_k -= w_k v and, in the same sweep, accumulates the NEXT
 //   column's partials x_{j+1}' a_k.  Lanes map to columns and loop over rows
@@ -47,27 +47,63 @@ int kSmemCap = 227 * 1024 - 1024;  // refined at first use (dyn_smem_cap)
 
 struct QrSmem {
     double* chunk;  // w columns x LD
-    double* ms1;    // [CS][slots] partial dots, reduce-scattered to the entry's owner
-    double* hd1;    // [slots] head-row entries for owned entries (from the row owner)
-    double* sa;     // [CS + 1] sigma partials (all-gathered) + alpha (slot CS)
-    double* wvb;    // [w] broadcast w_k values (index e = k - j)
-    double* red;    // [w] local combine scratch
+    double* msg;    // [2][CS][w] partial vectors, all-gathered with st.async
+    double* hrow;   // [2][w] head row (from the row owner)
+    double* red;    // [w] reduced entries of the current column / combine scratch
     double* part;   // [16][w] per-row-group partials
     double* hs;     // [4] house scalars: beta, tau, head, scale
+    uint64_t* bar;  // [2] mbarriers (one per message parity)
 };
 
 __device__ __forceinline__ QrSmem carve(double* sm, int w, int LD, int CS) {
-    const int slots = (w + CS - 1) / CS;
     QrSmem s;
     s.chunk = sm;
-    s.ms1 = s.chunk + static_cast<size_t>(w) * LD;
-    s.hd1 = s.ms1 + static_cast<size_t>(CS) * slots;
-    s.sa = s.hd1 + slots;
-    s.wvb = s.sa + CS + 1;
-    s.red = s.wvb + w;
+    s.msg = s.chunk + static_cast<size_t>(w) * LD;
+    s.hrow = s.msg + static_cast<size_t>(2) * CS * w;
+    s.red = s.hrow + static_cast<size_t>(2) * w;
     s.part = s.red + w;
     s.hs = s.part + static_cast<size_t>(kQrWarps) * w;
+    s.bar = reinterpret_cast<uint64_t*>(s.hs + 4);
     return s;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// Asynchronous remote store; completion is counted on the REMOTE mbarrier.
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+    uint64_t state;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                 : "=l"(state)
+                 : "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    (void)state;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
 }
 
 __device__ __forceinline__ int row_groups(int nk) {
@@ -77,11 +113,13 @@ __device__ __forceinline__ int row_groups(int nk) {
 
 // Fused pass.  Columns kc in [k0, w) (lanes <-> columns, 32 per column group,
 // warps split into column groups x row groups).  When upd0, columns >= kupd
-// get a -= wv[kc] * v_i on rows [iu, rc) (v = chunk column jv).  Every
-// column's dot with the NEXT column xn (chunk column jn, rows [id, rc),
-// id >= iu) is accumulated into part[rg][kc].
+// get a -= w_kc * v_i on rows [iu, rc) (v = chunk column jv), with
+// w_kc = tj * (hv[kc] + (scale ? dv[kc] / head : dv[kc])).  Every column's
+// dot with the NEXT column (chunk column jn, rows [id, rc), id >= iu) is
+// accumulated into part[rg][kc].
 __device__ __forceinline__ void fused_pass(const QrSmem& S, int LD, int w, int k0, int kupd, int rc,
-                                           bool upd0, int jv, int iu, const double* wv, int jn, int id) {
+                                           bool upd0, int jv, int iu, const double* hv, const double* dv,
+                                           double tj, double head, bool scale, int jn, int id) {
     const int nk = w - k0;
     if (nk <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -101,7 +139,8 @@ __device__ __forceinline__ void fused_pass(const QrSmem& S, int LD, int w, int k
     double acc0 = 0.0, acc1 = 0.0;
     if (upd) {
         const double* vcol = S.chunk + static_cast<size_t>(jv) * LD;
-        const double wk = wv[kc];
+        const double d = dv[kc];
+        const double wk = tj * (hv[kc] + (scale ? d / head : d));
         int i = rb;
         const int e1 = min(re, id);
         for (; i < e1; ++i) col[i] -= wk * vcol[i];  // rows in [iu, id): update only
@@ -136,7 +175,6 @@ __global__ void __launch_bounds__(kQrThreads, 1)
     const int rank = static_cast<int>(cluster.block_rank());
     extern __shared__ __align__(16) double sm[];
     const QrSmem S = carve(sm, w, LD, CS);
-    const int slots = (w + CS - 1) >> lcs;
     const int tid = threadIdx.x;
     const int r_beg = rank * R;
     const int rc = max(0, min(s, r_beg + R) - r_beg);  // my row count
@@ -146,18 +184,27 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             const int c = idx / rc, i = idx - c * rc;
             S.chunk[static_cast<size_t>(c) * LD + i] = A[(r_beg + i) + static_cast<int64_t>(c) * lda];
         }
-    if (CS > 1) cluster.sync(); else __syncthreads();  // all CTAs live before any DSMEM traffic
+    // message bytes for column c: CS partial vectors + the head row, (w - c) entries each
+    auto msg_bytes = [&](int c) { return static_cast<uint32_t>((CS + 1) * (w - c) * 8); };
+    if (tid == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (p > 0) mbar_arm(&S.bar[0], msg_bytes(0));
+        if (p > 1) mbar_arm(&S.bar[1], msg_bytes(1));
+    }
+    cluster.sync();  // every CTA live, barriers initialised, before any remote traffic
 
-    auto rmt = [&](double* local, int dst) { return CS > 1 ? cluster.map_shared_rank(local, dst) : local; };
-    auto bar = [&]() {
-        if (CS > 1) cluster.sync(); else __syncthreads();
-    };
+    const uint32_t msg_a = smem_u32(S.msg), hrow_a = smem_u32(S.hrow);
+    const uint32_t bar_a[2] = {smem_u32(&S.bar[0]), smem_u32(&S.bar[1])};
 
-    // Phase A for column jn: combine row-group partials, reduce-scatter entry
-    // e = k - jn to its owner (e % CS); all-gather the sigma partial; the row
-    // owner ships row jn: alpha to everyone, head entries to their owners.
-    auto phaseA = [&](int jn) {
-        const int nk = w - jn;
+    // All-gather of column jn's partials (and the row owner's row jn) into
+    // every CTA's msg/hrow slot of parity jn & 1, counted on its mbarrier.
+    auto send = [&](int jn) {
+        const int nk = w - jn, par = jn & 1;
         const int nrg = row_groups(nk);
         for (int e = tid; e < nk; e += kQrThreads) {
             double v = 0.0;
@@ -166,32 +213,35 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         }
         __syncthreads();
         const bool owner = jn >= r_beg && jn < r_beg + rc;
-        const double* hrow_src = S.chunk + (jn - r_beg);  // row jn: column c at hrow_src[c*LD]
+        const int jl = jn - r_beg;
         for (int e = tid; e < nk; e += kQrThreads) {
-            const int dst = e & (CS - 1), sl = e >> lcs;
-            rmt(S.ms1, dst)[static_cast<size_t>(rank) * slots + sl] = S.red[e];
-            if (owner) rmt(S.hd1, dst)[sl] = hrow_src[static_cast<size_t>(jn + e) * LD];
-        }
-        if (tid < CS) {
-            double* sa = rmt(S.sa, tid);
-            sa[rank] = S.red[0];
-            if (owner) sa[CS] = hrow_src[static_cast<size_t>(jn) * LD];
+            const double v = S.red[e];
+            const double h = owner ? S.chunk[static_cast<size_t>(jn + e) * LD + jl] : 0.0;
+            const uint32_t moff = msg_a + static_cast<uint32_t>(((par * CS + rank) * w + e) * 8);
+            const uint32_t hoff = hrow_a + static_cast<uint32_t>((par * w + e) * 8);
+            for (int dst = 0; dst < CS; ++dst) {
+                const uint32_t rbar = mapa_u32(bar_a[par], dst);
+                st_async_f64(mapa_u32(moff, dst), v, rbar);
+                if (owner) st_async_f64(mapa_u32(hoff, dst), h, rbar);
+            }
         }
     };
 
     if (p > 0) {  // initial partials for column 0 (dots over rows > 0)
-        fused_pass(S, LD, w, 0, w, rc, false, 0, 0, nullptr, 0, max(0, 1 - r_beg));
+        fused_pass(S, LD, w, 0, w, rc, false, 0, 0, nullptr, nullptr, 0.0, 1.0, false, 0, max(0, 1 - r_beg));
         __syncthreads();
-        phaseA(0);
+        send(0);
     }
 
     for (int j = 0; j < p; ++j) {
-        const int nk = w - j;
-        bar();  // (A) partials of column j visible at their owners
+        const int nk = w - j, par = j & 1;
+        mbar_wait(&S.bar[par], static_cast<uint32_t>((j >> 1) & 1));
+        const double* msgp = S.msg + static_cast<size_t>(par) * CS * w;
+        const double* hv = S.hrow + static_cast<size_t>(par) * w;  // hv[e] = a(j, j+e)
         if (tid < 32) {  // house() scalars (householder.cpp:20-34), one warp
             double sigma = 0.0;
-            for (int r = 0; r < CS; ++r) sigma += S.sa[r];
-            const double alpha = S.sa[CS];
+            for (int r = 0; r < CS; ++r) sigma += msgp[static_cast<size_t>(r) * w];
+            const double alpha = hv[0];
             double beta, tj, head = 1.0, scale = 0.0;
             if (sigma == 0.0) {
                 if (alpha >= 0.0) {
@@ -213,27 +263,24 @@ __global__ void __launch_bounds__(kQrThreads, 1)
                 S.hs[2] = head;
                 S.hs[3] = scale;
                 if (rank == 0) tau[j] = tj;
+                if (j + 2 < p) mbar_arm(&S.bar[par], msg_bytes(j + 2));  // next use of this slot
+            }
+        } else {
+            for (int e = tid - 32 + 1; e < nk; e += kQrThreads - 32) {  // reduce d_{j+e} in rank order
+                double d = 0.0;
+                for (int r = 0; r < CS; ++r) d += msgp[static_cast<size_t>(r) * w + e];
+                S.red[e] = d;
             }
         }
         __syncthreads();
         const double beta = S.hs[0], tj = S.hs[1], head = S.hs[2];
         const bool scale = S.hs[3] != 0.0;
-        // owned entries: w_k = tau (a(j,k) + d_k / head), broadcast to every CTA
-        for (int sl = tid; (sl << lcs) + rank < nk; sl += kQrThreads) {
-            const int e = (sl << lcs) + rank;
-            if (e == 0) continue;
-            double d = 0.0;
-            for (int r = 0; r < CS; ++r) d += S.ms1[static_cast<size_t>(r) * slots + sl];
-            const double wv = tj * (S.hd1[sl] + (scale ? d / head : d));
-            for (int dst = 0; dst < CS; ++dst) rmt(S.wvb, dst)[e] = wv;
-        }
-        bar();  // (B) w vector visible everywhere
         // row pass: scale the reflector, update column j+1 (rows > j) and row j
         const int iu = max(0, j + 1 - r_beg);
         double* xj = S.chunk + static_cast<size_t>(j) * LD;
         double* xn = S.chunk + static_cast<size_t>(j + 1) * LD;
-        const double w1 = nk > 1 ? S.wvb[1] : 0.0;
         const bool upd_next = nk > 1 && tj != 0.0;
+        const double w1 = nk > 1 ? tj * (hv[1] + (scale ? S.red[1] / head : S.red[1])) : 0.0;
         for (int i = iu + tid; i < rc; i += kQrThreads) {
             const double v = scale ? xj[i] / head : xj[i];
             xj[i] = v;
@@ -244,15 +291,19 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             const int jl = j - r_beg;
             if (tid == 0) xj[jl] = beta;
             if (tj != 0.0)
-                for (int e = 1 + tid; e < nk; e += kQrThreads) S.chunk[static_cast<size_t>(j + e) * LD + jl] -= S.wvb[e];
+                for (int e = 1 + tid; e < nk; e += kQrThreads) {
+                    const double d = S.red[e];
+                    S.chunk[static_cast<size_t>(j + e) * LD + jl] -= tj * (hv[e] + (scale ? d / head : d));
+                }
         }
         __syncthreads();
         if (j + 1 >= w) break;
         // fused pass: update columns j+2.. and accumulate the next partials
         // x_{j+1}' a_k over rows > j+1 (k = j+1 gives the next sigma).
-        fused_pass(S, LD, w, j + 1, j + 2, rc, tj != 0.0, j, iu, S.wvb - j, j + 1, max(0, j + 2 - r_beg));
+        fused_pass(S, LD, w, j + 1, j + 2, rc, tj != 0.0, j, iu, hv - j, S.red - j, tj, head, scale, j + 1,
+                   max(0, j + 2 - r_beg));
         __syncthreads();
-        if (j + 1 < p) phaseA(j + 1);
+        if (j + 1 < p) send(j + 1);
     }
 
     if (rc > 0)
@@ -260,13 +311,12 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             const int c = idx / rc, i = idx - c * rc;
             A[(r_beg + i) + static_cast<int64_t>(c) * lda] = S.chunk[static_cast<size_t>(c) * LD + i];
         }
-    if (CS > 1) cluster.sync();  // no CTA exits while a peer may still write into it
+    cluster.sync();  // no CTA exits while a peer may still write into it
 }
 
 size_t cluster_smem_bytes(int w, int LD, int cs) {
-    const size_t slots = (static_cast<size_t>(w) + cs - 1) / cs;
-    return (static_cast<size_t>(w) * LD + (static_cast<size_t>(cs) + 1) * slots + cs + 1 +
-            2 * static_cast<size_t>(w) + static_cast<size_t>(kQrWarps) * w + 4) *
+    return (static_cast<size_t>(w) * LD + static_cast<size_t>(2) * cs * w + 2 * static_cast<size_t>(w) +
+            static_cast<size_t>(w) + static_cast<size_t>(kQrWarps) * w + 4 + 2) *
            sizeof(double);
 }
 
