@@ -404,23 +404,36 @@ inline bool aligned16(const void* ptr, int64_t ld) {
 
 constexpr int kBK = 16;
 
-// Split-K factor for the small-tile config; 1 when the output tiles alone fill the chip.
-int choose_splits(int64_t M, int64_t N, int64_t K, int64_t work_elems) {
-    const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
-    const int64_t want_ctas = 3 * kNumSMs;
-    if (tiles >= want_ctas || K < 512) return 1;
-    int64_t sp = (want_ctas + tiles - 1) / tiles;
-    sp = std::min<int64_t>(sp, K / 256);
-    sp = std::min<int64_t>(sp, 32);
-    if (M * N > 0) sp = std::min<int64_t>(sp, work_elems / (M * N));
-    return static_cast<int>(std::max<int64_t>(sp, 1));
+// Tile config + split-K plan.  Large 128x128 tiles (8 warps, 1 CTA/SM) when
+// the output tiles -- times a split-K factor for long K -- fill about one
+// wave of 148 SMs; otherwise 64x64 tiles (several CTAs/SM) with split-K.
+struct GemmPlan {
+    bool large;
+    int splits;
+};
+
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t work_elems) {
+    const int64_t tl = ((M + 127) / 128) * ((N + 127) / 128);
+    if (tl >= kNumSMs) return {true, 1};
+    auto cap = [&](int64_t sp) {
+        if (M * N > 0) sp = std::min<int64_t>(sp, work_elems / (M * N));
+        return static_cast<int>(std::max<int64_t>(sp, 1));
+    };
+    // (128x128 tiles + split-K measured slower than 64x64 + split-K on the
+    // tall-skinny K = s products: one 8-warp CTA per SM hides less latency.)
+    const int64_t ts = ((M + 63) / 64) * ((N + 63) / 64);
+    const int64_t want = 3 * kNumSMs;
+    if (ts >= want || K < 512) return {false, 1};
+    int64_t sp = (want + ts - 1) / ts;
+    sp = std::min<int64_t>({sp, K / 128, 32});
+    return {false, cap(sp)};
 }
 
 }  // namespace
 
 int64_t gemm_work_elems(int64_t m, int64_t n, int64_t k) {
-    const int sp = choose_splits(m, n, k, INT64_MAX / 4);
-    return sp > 1 ? sp * m * n : 0;
+    const GemmPlan pl = plan_gemm(m, n, k, INT64_MAX / 4);
+    return pl.splits > 1 ? pl.splits * m * n : 0;
 }
 
 void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const DView& b,
@@ -447,12 +460,8 @@ void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const
     GemmParams p{M, N, K, a.data, a.ld, b.data, b.ld, c.data, c.ld, alpha, beta, work, K, 1};
     const bool vec = aligned16(a.data, a.ld) && aligned16(b.data, b.ld);
     const bool tA = ta == Op::T, tB = tb == Op::T;
-    const int64_t tiles_l = ((M + 127) / 128) * ((N + 127) / 128);
-    if (tiles_l >= kNumSMs) {
-        dispatch<128, 128, kBK, 64, 32, 3>(stream, p, tA, tB, vec, 1);
-        return;
-    }
-    int splits = work ? choose_splits(M, N, K, work_elems) : 1;
+    const GemmPlan pl = plan_gemm(M, N, K, work ? work_elems : 0);
+    int splits = work ? pl.splits : 1;
     if (splits > 1) {
         int64_t kc = (K + splits - 1) / splits;
         kc = (kc + kBK - 1) / kBK * kBK;
@@ -460,7 +469,36 @@ void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const
         p.kchunk = kc;
         p.splits = splits;
     }
-    dispatch<64, 64, kBK, 32, 32, 3>(stream, p, tA, tB, vec, splits);
+    if (pl.large)
+    {
+        static int cfg = [] {
+            const char* e = std::getenv("RUTV_GEMM_CFG");
+            return e ? std::atoi(e) : 2;
+        }();
+        // cfg 2 (16 warps of 32x32, BK = 32, 3 stages) measured best on B200:
+        // 27.9 TF/s at 8192^3 vs 24.4 for 8 warps of 64x32 (tools/gemmsweep.sh).
+        if (cfg == 1)
+            dispatch<128, 128, 16, 32, 32, 4>(stream, p, tA, tB, vec, splits);
+        else if (cfg == 0)
+            dispatch<128, 128, kBK, 64, 32, 3>(stream, p, tA, tB, vec, splits);
+        else
+            dispatch<128, 128, 32, 32, 32, 3>(stream, p, tA, tB, vec, splits);
+    }
+    else
+    {
+        static int scfg = [] {
+            const char* e = std::getenv("RUTV_GEMM_SCFG");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (scfg == 1)
+            dispatch<64, 64, 32, 32, 32, 3>(stream, p, tA, tB, vec, splits);
+        else if (scfg == 2)
+            dispatch<64, 64, 32, 32, 16, 3>(stream, p, tA, tB, vec, splits);
+        else if (scfg == 3)
+            dispatch<64, 64, 16, 32, 32, 4>(stream, p, tA, tB, vec, splits);
+        else
+            dispatch<64, 64, kBK, 32, 32, 3>(stream, p, tA, tB, vec, splits);
+    }
     if (splits > 1) {
         const int64_t total = M * N;
         const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));

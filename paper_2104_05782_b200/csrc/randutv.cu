@@ -154,15 +154,18 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
     }
     const int nsteps = static_cast<int>(plan.size());
 
-    cudaStream_t sB = st;
-    if (overlap) RUTV_CUDA(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
+    cudaStream_t sB = st, sC = st;
+    if (overlap) {
+        RUTV_CUDA(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
+        RUTV_CUDA(cudaStreamCreateWithFlags(&sC, cudaStreamNonBlocking));
+    }
     struct StreamGuard {
         cudaStream_t s;
         bool own;
         ~StreamGuard() {
             if (own) cudaStreamDestroy(s);
         }
-    } sguard{sB, overlap};
+    } sguard{sB, overlap}, sguardC{sC, overlap};
     std::vector<cudaEvent_t> events;
     struct EventGuard {
         std::vector<cudaEvent_t>& ev;
@@ -217,20 +220,27 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
         std::max<int64_t>({gemm_work_elems(n, bb, n), gemm_work_elems(bb, n, n), gemm_work_elems(vr + n, bb, n),
                            gemm_work_elems(bb, bb, n), gemm_work_elems(bb, n, bb), gemm_work_elems(vr + n, bb, bb),
                            1});
-    DevBuf GWA(gw_elems, st), GWB(gw_elems, st);
+    DevBuf GWA(gw_elems, st), GWB(gw_elems, st), GWC(gw_elems, st);
     const int64_t hqw = hqr_work_elems(n, bb);
     DevBuf HQ(hqw, st);
-    // allocations are stream-ordered on st; stream B must see them
-    wait(sB, record(st));
+    // allocations are stream-ordered on st; streams B and C must see them
+    {
+        const cudaEvent_t ev = record(st);
+        wait(sB, ev);
+        wait(sC, ev);
+    }
     // declared after every buffer -> destroyed first: stream B drains before any
     // buffer is released (also on the exception path)
     struct JoinGuard {
-        cudaStream_t s;
+        cudaStream_t s, c;
         bool own;
         ~JoinGuard() {
-            if (own) cudaStreamSynchronize(s);
+            if (own) {
+                cudaStreamSynchronize(s);
+                cudaStreamSynchronize(c);
+            }
         }
-    } jguard{sB, overlap};
+    } jguard{sB, sC, overlap};
 
     auto gemmA = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
                      const DView& c) { gemm(st, alpha, ta, a, tb, bm, beta, c, GWA.p, gw_elems); };
@@ -277,11 +287,19 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
         const cudaEvent_t evV = record(st);
         prof.mark(P_QRV);
         DView WvV(s, b, s, Wv[par]), MvV(s, b, s, Mv[par]);
-        {  // V-apply, critical rows: T22 (:140)
+        cudaEvent_t evR = nullptr;
+        {  // V-apply, critical rows: T22 (:140).  Panel-first look-ahead: the
+           // U-side QR only needs T22 Q_v's first b columns, so those are
+           // updated first on stream A and the other s-b columns on stream C,
+           // overlapping the panel QR.
             DView X = vt.block(vr + r0, r0, s, s);
             DView Zx(s, b, s, ZxA.p);
             gemmA(1.0, Op::N, X, Op::N, WvV, 0.0, Zx);
-            gemmA(-1.0, Op::N, Zx, Op::T, MvV, 1.0, X);
+            gemmA(-1.0, Op::N, Zx, Op::T, DView(b, b, s, Mv[par]), 1.0, X.block(0, 0, s, b));
+            wait(sC, record(st));
+            gemm(sC, -1.0, Op::N, Zx, Op::T, DView(s - b, b, s, Mv[par] + b), 1.0, X.block(0, b, s, s - b),
+                 GWC.p, gw_elems);
+            evR = record(sC);
         }
         prof.mark(P_APPLYV);
         // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
@@ -291,6 +309,7 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
         copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
         prof.mark(P_QRU);
         DView WuV(s, b, s, Wu[par]), MuV(s, b, s, Mu[par]);
+        wait(st, evR);
         {  // Q_u' on T22(:, b:) (:147)
             DView B = t22.block(0, b, s, s - b);
             DView Zl(b, s - b, b, ZlA.p);

@@ -88,3 +88,20 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f), errors="replace").read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), f
                 assert "rutv_oracle" not in txt and "librandutv_ref" not in txt, f
+
+
+def _build_shim(out):
+    import subprocess
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "shim_example.cpp"),
+           "-L", os.path.dirname(rutv.LIB_PATH), "-lrutv_b200",
+           f"-Wl,-rpath,{os.path.dirname(rutv.LIB_PATH)}", "-o", out]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return out
+
+
+def test_cpp_dropin_header_compiles_and_links(tmp_path):
+    """A reference-style C++ caller builds against include/randutv_b200/randutv.hpp
+    and links librutv_b200.so (the drop-in of randutv_blocked.hpp:39)."""
+    rutv.lib()
+    assert os.path.exists(_build_shim(str(tmp_path / "shim")))

@@ -118,3 +118,12 @@ def test_overlap_is_bit_identical():
         os.environ.pop("RUTV_OVERLAP")
     for x, y in zip(r1, r2):
         assert np.array_equal(x, y)
+
+
+def test_cpp_dropin_shim_runs(tmp_path):
+    import subprocess
+    from tests.test_capi import _build_shim
+    exe = _build_shim(str(tmp_path / "shim"))
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "config_error=1" in out.stdout
