@@ -153,6 +153,36 @@ int rutv_b200_gaussian_matrix(int device, int64_t m, int64_t n, uint64_t seed, d
 int rutv_b200_spectrum_matrix(int device, int64_t m, int64_t n, const double* sigma, double beta,
                               uint64_t seed, double* A, int64_t lda, rutv_status* st);
 
+/* ---------------- asynchronous building blocks (distributed driver) ----------------
+ * Enqueue on the calling thread's current stream (rutv_b200_set_stream; 0 =
+ * legacy default stream) and return without synchronising.  DEVICE pointers.
+ * Used by paper_2104_05782_b200/dist.py to compose a step of
+ * randutv_blocked.cpp:122-155 around NCCL collectives. */
+void rutv_b200_set_stream(uint64_t stream);
+int rutv_b200_gemm_async(double alpha, int ta, const double* A, int64_t ar, int64_t ac, int64_t lda, int tb,
+                         const double* B, int64_t br, int64_t bc, int64_t ldb, double beta, double* C, int64_t m,
+                         int64_t n, int64_t ldc, rutv_status* st);
+int rutv_b200_hqr_async(double* A, int64_t m, int64_t n, int64_t lda, double* tau, rutv_status* st);
+/* W (unit-lower), Twy and M = W Twy' of a packed QR (householder.cpp:37-44, 76-97). */
+int rutv_b200_form_wy(const double* qr, int64_t s, int64_t ldq, const double* tau, int64_t p, double* W,
+                      int64_t ldw, double* M, int64_t ldm, double* twy, int64_t ldt, rutv_status* st);
+int rutv_b200_normal_fill_async(uint64_t seed, uint64_t pos, double* G, int64_t rows, int64_t cols, int64_t ldg,
+                                rutv_status* st);
+int rutv_b200_copy_async(double* dst, int64_t rows, int64_t cols, int64_t ldd, const double* src, int64_t lds,
+                         rutv_status* st);
+int rutv_b200_copy_upper_async(double* dst, int64_t rows, int64_t cols, int64_t ldd, const double* src, int64_t lds,
+                               rutv_status* st);
+int rutv_b200_identity_async(double* a, int64_t rows, int64_t cols, int64_t lda, rutv_status* st);
+int rutv_b200_rect_diag_async(double* block, int64_t rows, int64_t cols, int64_t ld, const double* sigma, int64_t p,
+                              rutv_status* st);
+/* small rows [t*b, t*b+w) <-> big rows [(first + t*stride)*b, ...), t < count; scatter != 0 writes big. */
+int rutv_b200_block_rows_async(double* small, int64_t lds_small, double* big, int64_t ld_big, int64_t big_rows,
+                               int64_t cols, int64_t b, int64_t first, int64_t stride, int64_t count, int scatter,
+                               rutv_status* st);
+/* Batched svd_block over count square problems; status = device double[4*count]. */
+int rutv_b200_svd_batch_async(int count, const int64_t* n, double* const* A, const int64_t* lda, double* const* U,
+                              double* const* sigma, double* const* V, double* status, rutv_status* st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -260,3 +260,13 @@ def apply_qt_left(qr, twy, b) -> np.ndarray:
     _lib("port").ora_apply_qt_left(_p(qr), s, max(s, 1), _p(twy), p, _p(b), b.shape[1],
                                    max(b.shape[0], 1))
     return b
+
+
+def form_wy_t(qr, tau) -> np.ndarray:
+    """householder.cpp:76-97 on a packed QR: Twy (p x p)."""
+    qr = _f(qr)
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    p = tau.size
+    twy = np.zeros((p, p), order="F")
+    _lib("port").ora_form_wy_t(_p(qr), qr.shape[0], max(qr.shape[0], 1), _p(tau), p, _p(twy))
+    return twy

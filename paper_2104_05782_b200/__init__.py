@@ -98,6 +98,22 @@ def lib() -> C.CDLL:
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Status)]
     L.rutv_b200_normal_fill.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, _I64, _I64,
                                         _I64, C.POINTER(Status)]
+    # asynchronous building blocks (dist.py)
+    V, S = C.c_void_p, C.POINTER(Status)
+    L.rutv_b200_set_stream.argtypes = [C.c_uint64]
+    L.rutv_b200_set_stream.restype = None
+    L.rutv_b200_gemm_async.argtypes = [C.c_double, C.c_int, V, _I64, _I64, _I64, C.c_int, V, _I64, _I64, _I64,
+                                       C.c_double, V, _I64, _I64, _I64, S]
+    L.rutv_b200_hqr_async.argtypes = [V, _I64, _I64, _I64, V, S]
+    L.rutv_b200_form_wy.argtypes = [V, _I64, _I64, V, _I64, V, _I64, V, _I64, V, _I64, S]
+    L.rutv_b200_normal_fill_async.argtypes = [C.c_uint64, C.c_uint64, V, _I64, _I64, _I64, S]
+    L.rutv_b200_copy_async.argtypes = [V, _I64, _I64, _I64, V, _I64, S]
+    L.rutv_b200_copy_upper_async.argtypes = [V, _I64, _I64, _I64, V, _I64, S]
+    L.rutv_b200_identity_async.argtypes = [V, _I64, _I64, _I64, S]
+    L.rutv_b200_rect_diag_async.argtypes = [V, _I64, _I64, _I64, V, _I64, S]
+    L.rutv_b200_block_rows_async.argtypes = [V, _I64, V, _I64, _I64, _I64, _I64, _I64, _I64, _I64, C.c_int, S]
+    L.rutv_b200_svd_batch_async.argtypes = [C.c_int, C.POINTER(_I64), C.POINTER(V), C.POINTER(_I64),
+                                            C.POINTER(V), C.POINTER(V), C.POINTER(V), V, S]
     _lib = L
     return L
 

@@ -61,66 +61,72 @@ __global__ void copy_upper_kernel(int64_t rows, int64_t cols, double* d, int64_t
     }
 }
 
-// Twy (p x p, upper) from the Gram matrix G = W'W and tau, blocked by 32:
+// Twy (p x p, upper) from the Gram matrix G = W'W and tau, blocked by 32,
+// computed IN PLACE over G's strict upper triangle (column j of G is consumed
+// exactly when column j of T is produced):
 //   diagonal blocks: the reference recurrence T(k,j) = -tau_j sum_{l=k}^{j-1}
 //   T(k,l) G(l,j) (householder.cpp:84-95), one warp per block, lane k owning
-//   row k in registers;
+//   row k, the G column broadcast by warp shuffles;
 //   block column J: T(0:J0, J) = -T(0:J0, 0:J0) (G(0:J0, J) T_JJ), the
 //   standard two-block composition of compact-WY factors.
-// One CTA.  T lives in shared memory for p <= 128, else in the output buffer.
+// One CTA; the working array lives in shared memory for p <= 128 (one HBM
+// read of G, one write of T), else in the output buffer.
 __global__ void __launch_bounds__(1024) form_t_kernel(const double* __restrict__ gram, int64_t ldg,
                                                       const double* __restrict__ tau, int p,
                                                       double* t, int64_t ldt, int t_in_smem) {
     extern __shared__ __align__(16) double fsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* Ts = t_in_smem ? fsm : t;
+    double* M = t_in_smem ? fsm : t;
     const int64_t ld = t_in_smem ? p : ldt;
     double* Xs = fsm + (t_in_smem ? static_cast<size_t>(p) * p : 0);  // up to (p-32) x 32
     const int nblk = (p + 31) / 32;
-    // zero the strictly-lower part
     for (int64_t i = tid; i < static_cast<int64_t>(p) * p; i += blockDim.x) {
         const int64_t r = i % p, c = i / p;
-        if (r > c) Ts[r + c * ld] = 0.0;
+        M[r + c * ld] = r < c ? gram[r + c * ldg] : 0.0;
     }
-    // diagonal blocks
     __syncthreads();
-    if (warp < nblk) {  // lane k owns row I0 + k of the diagonal block
+    if (warp < nblk) {  // diagonal blocks: lane k owns row I0 + k
         const int I0 = warp * 32, bw = min(32, p - I0);
-        double* row = Ts + (I0 + lane);
+        double* row = M + (I0 + lane);
         for (int j = 0; j < bw; ++j) {
             const double tj = tau[I0 + j];
-            const double* gcol = gram + I0 + static_cast<int64_t>(I0 + j) * ldg;
+            double* colj = M + static_cast<int64_t>(I0 + j) * ld + I0;
+            const double zl = lane < j ? colj[lane] : 0.0;  // G(I0+lane, I0+j)
+            __syncwarp();
             double s = 0.0;
-            for (int l = lane; l < j; ++l) s += row[static_cast<int64_t>(I0 + l) * ld] * gcol[l];
-            if (lane < j) row[static_cast<int64_t>(I0 + j) * ld] = -tj * s;
-            else if (lane == j) row[static_cast<int64_t>(I0 + j) * ld] = tj;
+            for (int l = 0; l < j; ++l) {
+                const double z = __shfl_sync(0xffffffffu, zl, l);
+                if (l >= lane) s += row[static_cast<int64_t>(I0 + l) * ld] * z;
+            }
+            if (lane < j) colj[lane] = -tj * s;
+            else if (lane == j) colj[lane] = tj;
+            __syncwarp();
         }
     }
     __syncthreads();
-    // off-diagonal block columns
-    for (int J = 1; J < nblk; ++J) {
+    for (int J = 1; J < nblk; ++J) {  // off-diagonal block columns
         const int J0 = J * 32, bw = min(32, p - J0);
         const int cnt = J0 * bw;
         for (int e = tid; e < cnt; e += blockDim.x) {  // X = G(0:J0, J) T_JJ
             const int r = e % J0, c = e / J0;
             double s = 0.0;
             for (int l = 0; l <= c; ++l)
-                s += gram[r + static_cast<int64_t>(J0 + l) * ldg] * Ts[(J0 + l) + static_cast<int64_t>(J0 + c) * ld];
+                s += M[r + static_cast<int64_t>(J0 + l) * ld] * M[(J0 + l) + static_cast<int64_t>(J0 + c) * ld];
             Xs[r + static_cast<size_t>(c) * J0] = s;
         }
         __syncthreads();
         for (int e = tid; e < cnt; e += blockDim.x) {  // T(0:J0, J) = -T(0:J0, 0:J0) X
             const int r = e % J0, c = e / J0;
             double s = 0.0;
-            for (int m = r; m < J0; ++m) s += Ts[r + static_cast<int64_t>(m) * ld] * Xs[m + static_cast<size_t>(c) * J0];
-            Ts[r + static_cast<int64_t>(J0 + c) * ld] = -s;
+            for (int m = r; m < J0; ++m) s += M[r + static_cast<int64_t>(m) * ld] * Xs[m + static_cast<size_t>(c) * J0];
+            M[r + static_cast<int64_t>(J0 + c) * ld] = -s;
         }
         __syncthreads();
     }
     if (t_in_smem)
         for (int64_t i = tid; i < static_cast<int64_t>(p) * p; i += blockDim.x) {
             const int64_t r = i % p, c = i / p;
-            t[r + c * ldt] = Ts[r + c * p];
+            t[r + c * ldt] = M[r + c * p];
         }
 }
 
