@@ -61,7 +61,7 @@ __device__ __forceinline__ void rr_pair(int N, int r, int pi, int& p, int& q) {
 
 template <int RPL>
 __global__ void __launch_bounds__(kJThreads, 1)
-    jacobi_kernel(const SvdDesc* __restrict__ descs, int R, int vsm, double tol, int max_sweeps) {
+    jacobi_kernel(const SvdDesc* __restrict__ descs, int R, int vsm, int rs, double tol, int max_sweeps) {
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = static_cast<int>(cluster.num_blocks());
     const int rank = static_cast<int>(cluster.block_rank());
@@ -129,16 +129,51 @@ __global__ void __launch_bounds__(kJThreads, 1)
         return;
     }
 
-    // Phase 1 of a round: partial (alpha, beta, gamma) of every pair over my rows.
-    auto phase1 = [&](int r, int par) {
+    // One round.  mode 0: rotate; mode 1: check only (owners track the worst
+    // remaining pair ratio).  All-gather exchange (rs == 0): every CTA gets every
+    // pair's partials and decides itself -- one cluster barrier.  Reduce-scatter
+    // (rs != 0, large clusters): pair pi's partials go to CTA pi % CS, which
+    // decides and broadcasts (c, s, flag) -- two barriers, O(npairs) words.
+    const int slots = (npairs + CS - 1) / CS;
+    double* dec = xb + static_cast<size_t>(CS) * slots * 3;  // rs mode: [npairs][3]
+    auto decide = [&](double al, double be, double ga, double& c, double& s, double& ratio) -> bool {
+        const double np = sqrt(al), nq = sqrt(be);
+        ratio = -1.0;
+        if (np <= floor_col || nq <= floor_col) return false;
+        ratio = fabs(ga) / (np * nq);
+        if (fabs(ga) <= rel * np * nq) return false;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        c = 1.0 / sqrt(1.0 + tt * tt);
+        s = c * tt;
+        return true;
+    };
+    auto rotate = [&](int p, int q, double c, double s) {
+        double* bp = Bs + static_cast<size_t>(p) * R;
+        double* bq = Bs + static_cast<size_t>(q) * R;
+        double* vp = Vs + static_cast<size_t>(p) * R;
+        double* vq = Vs + static_cast<size_t>(q) * R;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+            const int i = sl + kLPP * t;
+            if (i < r_cnt) {
+                const double x = bp[i], y = bq[i], vx = vp[i], vy = vq[i];
+                bp[i] = c * x - s * y;
+                bq[i] = s * x + c * y;
+                vp[i] = c * vx - s * vy;
+                vq[i] = s * vx + c * vy;
+            }
+        }
+    };
+    auto round = [&](int r, int par, int mode, double& worst) -> bool {
+        // phase 1: partial dots of every pair over my rows
         for (int base = 0; base < npairs; base += kPairsPerPass) {
             const int pi = base + warp * kPPW + grp;
             int p = 0, q = 0;
             const bool ok = pi < npairs;
             if (ok) rr_pair(N, r, pi, p, q);
-            const bool real = ok && q < n;
             double a = 0.0, b = 0.0, g = 0.0;
-            if (real) {
+            if (ok && q < n) {
                 const double* cp = Bs + static_cast<size_t>(p) * R;
                 const double* cq = Bs + static_cast<size_t>(q) * R;
 #pragma unroll
@@ -158,109 +193,130 @@ __global__ void __launch_bounds__(kJThreads, 1)
                 b += __shfl_xor_sync(0xffffffffu, b, o);
                 g += __shfl_xor_sync(0xffffffffu, g, o);
             }
-            if (ok) {
-                if (CS == 1) {
-                    if (sl == 0) {
-                        double* slot = xb + par * xpar + static_cast<size_t>(pi) * 3;
-                        slot[0] = a;
-                        slot[1] = b;
-                        slot[2] = g;
-                    }
-                } else {
-                    for (int dst = sl; dst < CS; dst += kLPP) {
-                        double* slot = cluster.map_shared_rank(xb, dst) + par * xpar +
-                                       (static_cast<size_t>(rank) * npairs + pi) * 3;
-                        slot[0] = a;
-                        slot[1] = b;
-                        slot[2] = g;
-                    }
+            if (!ok) continue;
+            if (rs) {
+                if (sl == 0) {
+                    double* slot = cluster.map_shared_rank(xb, pi % CS) +
+                                   (static_cast<size_t>(rank) * slots + pi / CS) * 3;
+                    slot[0] = a;
+                    slot[1] = b;
+                    slot[2] = g;
+                }
+            } else if (CS == 1) {
+                if (sl == 0) {
+                    double* slot = xb + par * xpar + static_cast<size_t>(pi) * 3;
+                    slot[0] = a;
+                    slot[1] = b;
+                    slot[2] = g;
+                }
+            } else {
+                for (int dst = sl; dst < CS; dst += kLPP) {
+                    double* slot = cluster.map_shared_rank(xb, dst) + par * xpar +
+                                   (static_cast<size_t>(rank) * npairs + pi) * 3;
+                    slot[0] = a;
+                    slot[1] = b;
+                    slot[2] = g;
                 }
             }
         }
+        if (CS > 1) cluster.sync(); else __syncthreads();
+        bool any = false;
+        if (rs) {
+            // owners reduce their pairs in rank order and broadcast the decision
+            for (int k = tid; k < slots; k += kJThreads) {
+                const int pi = rank + k * CS;
+                if (pi >= npairs) continue;
+                int p, q;
+                rr_pair(N, r, pi, p, q);
+                double c = 1.0, s = 0.0, flag = 0.0, ratio = -1.0;
+                if (q < n) {
+                    double al = 0.0, be = 0.0, ga = 0.0;
+                    for (int rr = 0; rr < CS; ++rr) {
+                        const double* slot = xb + (static_cast<size_t>(rr) * slots + k) * 3;
+                        al += slot[0];
+                        be += slot[1];
+                        ga += slot[2];
+                    }
+                    if (decide(al, be, ga, c, s, ratio) && mode == 0) flag = 1.0;
+                    if (mode == 1 && ratio >= 0.0) worst = fmax(worst, ratio);
+                }
+                for (int dst = 0; dst < CS; ++dst) {
+                    double* dd = cluster.map_shared_rank(dec, dst) + 3 * pi;
+                    dd[0] = c;
+                    dd[1] = s;
+                    dd[2] = flag;
+                }
+            }
+            cluster.sync();
+            if (mode == 0)
+                for (int base = 0; base < npairs; base += kPairsPerPass) {
+                    const int pi = base + warp * kPPW + grp;
+                    if (pi >= npairs) continue;
+                    const double* dd = dec + 3 * pi;
+                    if (dd[2] == 0.0) continue;
+                    int p, q;
+                    rr_pair(N, r, pi, p, q);
+                    any = true;
+                    rotate(p, q, dd[0], dd[1]);
+                }
+        } else {
+            for (int base = 0; base < npairs; base += kPairsPerPass) {
+                const int pi = base + warp * kPPW + grp;
+                if (pi >= npairs) continue;
+                int p, q;
+                rr_pair(N, r, pi, p, q);
+                if (q >= n) continue;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int rr = 0; rr < CS; ++rr) {
+                    const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
+                    al += slot[0];
+                    be += slot[1];
+                    ga += slot[2];
+                }
+                double c, s, ratio;
+                const bool rot = decide(al, be, ga, c, s, ratio);
+                if (mode == 1) {
+                    if (ratio >= 0.0) worst = fmax(worst, ratio);
+                    continue;
+                }
+                if (!rot) continue;
+                any = true;
+                rotate(p, q, c, s);
+            }
+        }
+        __syncthreads();
+        return any;
     };
 
     bool converged = false;
     int sweep = 0;
     int par = 0;
+    double worst = 0.0;
     for (; sweep < max_sweeps && !converged; ++sweep) {
         if (tid == 0) s_rot = 0;
-        for (int r = 0; r < N - 1; ++r, par ^= 1) {
-            phase1(r, par);
-            if (CS > 1) cluster.sync(); else __syncthreads();
-            bool any = false;
-            for (int base = 0; base < npairs; base += kPairsPerPass) {
-                const int pi = base + warp * kPPW + grp;
-                if (pi >= npairs) continue;
-                int p, q;
-                rr_pair(N, r, pi, p, q);
-                if (q >= n) continue;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int rr = 0; rr < CS; ++rr) {
-                    const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
-                    al += slot[0];
-                    be += slot[1];
-                    ga += slot[2];
-                }
-                const double np = sqrt(al), nq = sqrt(be);
-                if (np <= floor_col || nq <= floor_col) continue;
-                if (fabs(ga) <= rel * np * nq) continue;
-                const double zeta = (be - al) / (2.0 * ga);
-                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + tt * tt);
-                const double s = c * tt;
-                any = true;
-                double* bp = Bs + static_cast<size_t>(p) * R;
-                double* bq = Bs + static_cast<size_t>(q) * R;
-                double* vp = Vs + static_cast<size_t>(p) * R;
-                double* vq = Vs + static_cast<size_t>(q) * R;
-#pragma unroll
-                for (int t = 0; t < RPL; ++t) {
-                    const int i = sl + kLPP * t;
-                    if (i < r_cnt) {
-                        const double x = bp[i], y = bq[i], vx = vp[i], vy = vq[i];
-                        bp[i] = c * x - s * y;
-                        bq[i] = s * x + c * y;
-                        vp[i] = c * vx - s * vy;
-                        vq[i] = s * vx + c * vy;
-                    }
-                }
-            }
-            if (any) s_rot = 1;
-            __syncthreads();
-        }
+        __syncthreads();
+        for (int r = 0; r < N - 1; ++r, par ^= 1)
+            if (round(r, par, 0, worst)) s_rot = 1;
+        __syncthreads();
         converged = s_rot == 0;
         __syncthreads();
     }
 
     if (!converged) {  // residual: worst remaining pair ratio (jacobi_svd.cpp:97-109)
-        double worst = 0.0;
-        for (int r = 0; r < N - 1; ++r, par ^= 1) {
-            phase1(r, par);
-            if (CS > 1) cluster.sync(); else __syncthreads();
-            for (int base = 0; base < npairs; base += kPairsPerPass) {
-                const int pi = base + warp * kPPW + grp;
-                if (pi >= npairs) continue;
-                int p, q;
-                rr_pair(N, r, pi, p, q);
-                if (q >= n) continue;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int rr = 0; rr < CS; ++rr) {
-                    const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
-                    al += slot[0];
-                    be += slot[1];
-                    ga += slot[2];
-                }
-                const double np = sqrt(al), nq = sqrt(be);
-                if (!(np <= floor_col || nq <= floor_col)) worst = fmax(worst, fabs(ga) / (np * nq));
-            }
-            __syncthreads();
-        }
+        for (int r = 0; r < N - 1; ++r, par ^= 1) round(r, par, 1, worst);
         for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
         if (lane == 0) s_red[warp] = worst;
         __syncthreads();
-        if (rank == 0 && tid == 0) {
+        if (tid == 0) {
             double m = 0.0;
             for (int w = 0; w < nwarps; ++w) m = fmax(m, s_red[w]);
+            if (CS > 1) cluster.map_shared_rank(xb, 0)[rank] = m;
+            else xb[0] = m;
+        }
+        if (CS > 1) cluster.sync(); else __syncthreads();
+        if (rank == 0 && tid == 0) {
+            double m = 0.0;
+            for (int r = 0; r < CS; ++r) m = fmax(m, xb[r]);
             d.status[0] = RUTV_ERR_CONVERGENCE;
             d.status[1] = m;
             d.status[2] = n;
@@ -414,9 +470,14 @@ void jinit() {
     cudaGetLastError();
 }
 
+bool use_rs(int n, int cs) { return cs >= 8 && n > 256; }
+
 size_t jsmem_bytes(int n, int R, int cs, bool vsm) {
     const int npairs = (n + (n & 1)) / 2;
-    const size_t x = std::max<size_t>(2 * static_cast<size_t>(cs) * npairs * 3, static_cast<size_t>(cs) * n + 8);
+    const size_t slots = (static_cast<size_t>(npairs) + cs - 1) / cs;
+    const size_t xg = use_rs(n, cs) ? static_cast<size_t>(cs) * slots * 3 + 3 * static_cast<size_t>(npairs)
+                                    : 2 * static_cast<size_t>(cs) * npairs * 3;
+    const size_t x = std::max<size_t>(xg, static_cast<size_t>(cs) * n + 8);
     return (static_cast<size_t>(n) * R * (vsm ? 2 : 1) + x) * sizeof(double);
 }
 
@@ -451,6 +512,7 @@ void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax,
                int max_sweeps) {
     if (count <= 0) return;
     const JCfg c = choose(nmax);
+    const int rs = use_rs(nmax, c.cs) ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(count * c.cs));
     cfg.blockDim = dim3(kJThreads);
@@ -464,10 +526,10 @@ void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax,
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     switch (c.rpl) {
-        case 2: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<2>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
-        case 4: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<4>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
-        case 8: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<8>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
-        default: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<16>, d_descs, c.R, c.vsm, tol, max_sweeps)); break;
+        case 2: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<2>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
+        case 4: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<4>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
+        case 8: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<8>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
+        default: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<16>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
     }
     note_launch();
     complete_kernel<<<count, 256, 0, stream>>>(d_descs);

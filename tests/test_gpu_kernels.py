@@ -163,7 +163,7 @@ def _svd_dev(a, **kw):
     return to_np(U), s.cpu().numpy()[:n], to_np(V)
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 16, 63, 128, 129, 256])
+@pytest.mark.parametrize("n", [1, 2, 5, 16, 63, 128, 129, 256, 336, 512])
 def test_svd_block_reconstructs(n):
     a = _rand(n, n, 200 + n)
     u, s, v = _svd_dev(a)
