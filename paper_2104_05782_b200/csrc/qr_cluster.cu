@@ -106,10 +106,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-__device__ __forceinline__ int row_groups(int nk) {
-    const int ncg = (nk + 31) >> 5;
-    return ncg >= 16 ? 1 : kQrWarps / ncg;
+__device__ __forceinline__ int col_groups_log(int nk) {
+    const int ncg = (nk + 31) >> 5;  // 32 columns (lanes) per group, rounded up to a power of two
+    return ncg <= 1 ? 0 : ncg <= 2 ? 1 : ncg <= 4 ? 2 : ncg <= 8 ? 3 : 4;
 }
+__device__ __forceinline__ int row_groups(int nk) { return max(1, kQrWarps >> col_groups_log(nk)); }
 
 // Fused pass.  Columns kc in [k0, w) (lanes <-> columns, 32 per column group,
 // warps split into column groups x row groups).  When upd0, columns >= kupd
@@ -119,20 +120,21 @@ __device__ __forceinline__ int row_groups(int nk) {
 // accumulated into part[rg][kc].
 __device__ __forceinline__ void fused_pass(const QrSmem& S, int LD, int w, int k0, int kupd, int rc,
                                            bool upd0, int jv, int iu, const double* hv, const double* dv,
-                                           double tj, double head, bool scale, int jn, int id) {
+                                           double tj, double rh, bool scale, int jn, int id) {
     const int nk = w - k0;
     if (nk <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ncg = (nk + 31) >> 5;
-    const int nrg = row_groups(nk);
-    const int rg = warp / ncg, cg_ = warp - rg * ncg;
+    const int lcg = col_groups_log(nk);
+    const int lnrg = max(0, 4 - lcg);  // log2(kQrWarps) = 4
+    const int nrg = 1 << lnrg;
+    const int rg = warp >> lcg, cg_ = warp & ((1 << lcg) - 1);
     if (rg >= nrg) return;
     const int kc = k0 + cg_ * 32 + lane;
     if (kc >= w) return;
     const bool upd = upd0 && kc >= kupd;
     const int lo = upd0 ? iu : id;
     const int span = max(0, rc - lo);
-    const int per = (span + nrg - 1) / nrg;
+    const int per = (span + nrg - 1) >> lnrg;
     const int rb = lo + rg * per, re = min(rc, rb + per);
     double* col = S.chunk + static_cast<size_t>(kc) * LD;
     const double* ncol = S.chunk + static_cast<size_t>(jn) * LD;
@@ -140,30 +142,40 @@ __device__ __forceinline__ void fused_pass(const QrSmem& S, int LD, int w, int k
     if (upd) {
         const double* vcol = S.chunk + static_cast<size_t>(jv) * LD;
         const double d = dv[kc];
-        const double wk = tj * (hv[kc] + (scale ? d / head : d));
+        const double wk = tj * (hv[kc] + (scale ? d * rh : d));
         int i = rb;
         const int e1 = min(re, id);
         for (; i < e1; ++i) col[i] -= wk * vcol[i];  // rows in [iu, id): update only
-        for (; i + 1 < re; i += 2) {
-            const double a0 = col[i] - wk * vcol[i];
-            const double a1 = col[i + 1] - wk * vcol[i + 1];
-            col[i] = a0;
-            col[i + 1] = a1;
-            acc0 += ncol[i] * a0;
-            acc1 += ncol[i + 1] * a1;
+        double* cp = col + i;
+        const double* vp = vcol + i;
+        const double* np = ncol + i;
+        const int cntr = re - i;
+        int t = 0;
+#pragma unroll 1
+        for (; t + 3 < cntr; t += 4) {
+            const double a0 = cp[t] - wk * vp[t];
+            const double a1 = cp[t + 1] - wk * vp[t + 1];
+            const double a2 = cp[t + 2] - wk * vp[t + 2];
+            const double a3 = cp[t + 3] - wk * vp[t + 3];
+            cp[t] = a0;
+            cp[t + 1] = a1;
+            cp[t + 2] = a2;
+            cp[t + 3] = a3;
+            acc0 += np[t] * a0 + np[t + 2] * a2;
+            acc1 += np[t + 1] * a1 + np[t + 3] * a3;
         }
-        if (i < re) {
-            const double a0 = col[i] - wk * vcol[i];
-            col[i] = a0;
-            acc0 += ncol[i] * a0;
+        for (; t < cntr; ++t) {
+            const double a0 = cp[t] - wk * vp[t];
+            cp[t] = a0;
+            acc0 += np[t] * a0;
         }
     } else {
         int i = max(rb, id);
-        for (; i + 1 < re; i += 2) {
-            acc0 += ncol[i] * col[i];
-            acc1 += ncol[i + 1] * col[i + 1];
+        for (; i + 3 < re; i += 4) {
+            acc0 += ncol[i] * col[i] + ncol[i + 2] * col[i + 2];
+            acc1 += ncol[i + 1] * col[i + 1] + ncol[i + 3] * col[i + 3];
         }
-        if (i < re) acc0 += ncol[i] * col[i];
+        for (; i < re; ++i) acc0 += ncol[i] * col[i];
     }
     S.part[static_cast<size_t>(rg) * w + kc] = acc0 + acc1;
 }
@@ -275,12 +287,13 @@ __global__ void __launch_bounds__(kQrThreads, 1)
         __syncthreads();
         const double beta = S.hs[0], tj = S.hs[1], head = S.hs[2];
         const bool scale = S.hs[3] != 0.0;
+        const double rh = 1.0 / head;  // w_k uses d_k * (1/head); v keeps the reference's division
         // row pass: scale the reflector, update column j+1 (rows > j) and row j
         const int iu = max(0, j + 1 - r_beg);
         double* xj = S.chunk + static_cast<size_t>(j) * LD;
         double* xn = S.chunk + static_cast<size_t>(j + 1) * LD;
         const bool upd_next = nk > 1 && tj != 0.0;
-        const double w1 = nk > 1 ? tj * (hv[1] + (scale ? S.red[1] / head : S.red[1])) : 0.0;
+        const double w1 = nk > 1 ? tj * (hv[1] + (scale ? S.red[1] * rh : S.red[1])) : 0.0;
         for (int i = iu + tid; i < rc; i += kQrThreads) {
             const double v = scale ? xj[i] / head : xj[i];
             xj[i] = v;
@@ -293,14 +306,14 @@ __global__ void __launch_bounds__(kQrThreads, 1)
             if (tj != 0.0)
                 for (int e = 1 + tid; e < nk; e += kQrThreads) {
                     const double d = S.red[e];
-                    S.chunk[static_cast<size_t>(j + e) * LD + jl] -= tj * (hv[e] + (scale ? d / head : d));
+                    S.chunk[static_cast<size_t>(j + e) * LD + jl] -= tj * (hv[e] + (scale ? d * rh : d));
                 }
         }
         __syncthreads();
         if (j + 1 >= w) break;
         // fused pass: update columns j+2.. and accumulate the next partials
         // x_{j+1}' a_k over rows > j+1 (k = j+1 gives the next sigma).
-        fused_pass(S, LD, w, j + 1, j + 2, rc, tj != 0.0, j, iu, hv - j, S.red - j, tj, head, scale, j + 1,
+        fused_pass(S, LD, w, j + 1, j + 2, rc, tj != 0.0, j, iu, hv - j, S.red - j, tj, rh, scale, j + 1,
                    max(0, j + 2 - r_beg));
         __syncthreads();
         if (j + 1 < p) send(j + 1);
