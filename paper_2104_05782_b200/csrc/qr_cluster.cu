@@ -32,7 +32,10 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
+#include "cluster_msg.cuh"
 #include "rutv_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -65,45 +68,6 @@ __device__ __forceinline__ QrSmem carve(double* sm, int w, int LD, int CS) {
     s.hs = s.part + static_cast<size_t>(kQrWarps) * w;
     s.bar = reinterpret_cast<uint64_t*>(s.hs + 4);
     return s;
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    return r;
-}
-// Asynchronous remote store; completion is counted on the REMOTE mbarrier.
-__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
-                 "r"(rbar)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
-    uint64_t state;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
-                 : "=l"(state)
-                 : "r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    (void)state;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-    }
 }
 
 __device__ __forceinline__ int col_groups_log(int nk) {
@@ -419,19 +383,48 @@ int64_t hqr_work_elems(int64_t s, int64_t w) {
            gemm_work_elems(nb, nb, s) + 1024;
 }
 
+// qr_reg.cu: micro-panel register kernel (preferred where its chunk fits)
+int qr_reg_capacity(int64_t s, int cs);
+int qr_reg_rows();
+void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs);
+
+namespace {
+bool reg_kernel_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RUTV_QR_KERNEL");
+        return !(e && std::string(e) == "cluster");
+    }();
+    return on;
+}
+}  // namespace
+
 void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, int64_t ldt,
                double* scratch, int64_t scratch_elems) {
     const int64_t s = a.rows, w = a.cols, p = std::min(s, w);
     if (p == 0) return;
     const int cmax = max_cluster();
-    const int cap = cluster_cols_capacity(s, cmax);
+    const bool use_reg = reg_kernel_enabled() && qr_reg_capacity(s, cmax) >= std::min<int64_t>(w, 16);
+    auto pick_reg = [&](int64_t rows, int64_t cols) {
+        int cs = 1;
+        while (cs < cmax && (rows + cs - 1) / cs > qr_reg_rows()) cs *= 2;
+        while (cs < cmax && qr_reg_capacity(rows, cs) < cols) cs *= 2;
+        return cs;
+    };
+    auto launch = [&](const DView& sub, double* t) {
+        if (use_reg)
+            qr_reg_launch(stream, sub, t, pick_reg(sub.rows, sub.cols));
+        else
+            launch_cluster(stream, sub, t, pick_cluster(sub.rows, sub.cols, cmax));
+    };
+    int cap = use_reg ? qr_reg_capacity(s, cmax) : cluster_cols_capacity(s, cmax);
     if (cap < 1) throw Error(RUTV_ERR_NOTIMPL, "hqr: panel too tall for one cluster");
+    if (use_reg && cap >= 16 && cap < w) cap = cap / 16 * 16;
     if (cap >= w && w <= 512) {
-        launch_cluster(stream, a, tau, pick_cluster(s, w, cmax));
+        launch(a, tau);
     } else {
         // Blocked right-looking: sub-panels of nb columns, trailing update
         // A_trail <- (I - W T W')' A_trail = A_trail - W T' (W' A_trail).
-        const int64_t nb = std::min<int64_t>(512, std::max<int64_t>(1, (cap / 8) * 8 > 0 ? (cap / 8) * 8 : cap));
+        const int64_t nb = std::min<int64_t>(512, use_reg ? cap : std::max<int64_t>(1, (cap / 8) * 8 > 0 ? (cap / 8) * 8 : cap));
         double* W = scratch;
         double* Gm = W + s * nb;
         double* Ts = Gm + nb * nb;
@@ -442,7 +435,7 @@ void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, in
         for (int64_t j0 = 0; j0 < p; j0 += nb) {
             const int64_t jb = std::min(nb, p - j0);
             DView sub = a.block(j0, j0, s - j0, jb);
-            launch_cluster(stream, sub, tau + j0, pick_cluster(s - j0, jb, cmax));
+            launch(sub, tau + j0);
             const int64_t rest = w - j0 - jb;
             if (rest <= 0) continue;
             DView trail = a.block(j0, j0 + jb, s - j0, rest);

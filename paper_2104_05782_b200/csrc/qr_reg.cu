@@ -1,0 +1,595 @@
+// qr_reg.cu -- Householder panel QR on a thread-block cluster, micro-panels in
+// registers (sm_100a DSMEM + DMMA).
+//
+// Same arithmetic contract as qr_cluster.cu: the reference's house() convention
+// (proj/src/householder.cpp:20-34, beta >= 0, Parlett head, tau = 2 sign flip,
+// tau = 0 skip) and hqr_inplace's left-to-right reflector order
+// (householder.cpp:48-67); outputs are the packed R / unit-lower V and tau.
+//
+// Why a second kernel: the one-level kernel streams every trailing column of
+// the panel through shared memory once per column (3 loads + 1 store per
+// element per column), which makes a 128-column panel shared-memory-bandwidth
+// and latency bound at 3.5-9 us per column.  Here the panel is processed in
+// micro-panels of KB = 16 columns:
+//
+//   * the s x w panel is split by rows over CS CTAs (one cluster); each CTA
+//     keeps its row chunk resident in shared memory (odd leading dimension);
+//   * the current micro-panel lives in REGISTERS: thread t owns local rows
+//     t, t + 512, ... and all 16 columns of them.  Per column j the thread
+//     scales its reflector entry, applies the reflector to its 15 other
+//     columns and accumulates its share of the next column's dot products --
+//     no shared-memory traffic at all;
+//   * the 16 partial dots (and the owner's head row) are reduced by a warp
+//     butterfly, then across warps, then all-gathered over the cluster with
+//     st.async remote stores completing on the receivers' mbarriers (one DSMEM
+//     hop per column); every CTA sums the CS partials in rank order, so all
+//     CTAs hold bit-identical house() scalars;
+//   * after each micro-panel the trailing columns of the panel receive the
+//     block reflector, Q' A_t = A_t - V T' (V' A_t): V'[V | A_t] is formed with
+//     warp-level DMMA (mma.sync m16n8k4 f64), reduce-scattered and all-gathered
+//     over the cluster (deterministic rank order), T comes from the Gram
+//     matrix V'V and tau by the forward recurrence of form_wy_t
+//     (householder.cpp:69-97), and the rank-16 update is again DMMA.
+//
+// Rows per thread MR = 1 or 2 (chunk rows R <= 1024); taller chunks use the
+// one-level kernel.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "cluster_msg.cuh"
+#include "rutv_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rutv {
+
+namespace {
+
+constexpr int kT = 512;       // threads per CTA
+constexpr int kWarps = kT / 32;
+constexpr int KB = 16;        // micro-panel width
+constexpr int kMsg = 2 * KB;  // per-column message: 16 partial dots + 16 head-row entries
+constexpr unsigned kFull = 0xffffffffu;
+
+struct RegSmem {
+    double* chunk;  // w x LD, column-major
+    double* msg;    // [2][CS][kMsg]
+    double* rsb;    // [CS][KB][nsmax] reduce-scatter inbox
+    double* zg;     // [KB][ncol] all-gathered V'[V | A_t], then -T'Z in place
+    double* part;   // per-warp partials: column dots [kWarps][KB]; block [ksplit][KB][ncol]
+    double* tmat;   // [KB][KB] T, row-major
+    double* taus;   // [KB]
+    double* hsend;  // [KB] head row of the next column (row owner only)
+    double* wks;    // [KB] w_k of the current column (k = 1..15, window-relative)
+    double* hs;     // [4] beta, 1/head (or 1), tau
+    uint64_t* bar;  // [4]: column parity 0/1, reduce-scatter, all-gather
+};
+
+__host__ __device__ inline int ns_max(int w, int cs) { return (KB + w + cs - 1) / cs; }
+__host__ __device__ inline int part_elems(int w) { return KB * std::max(kWarps * 8, KB + w); }
+
+__host__ __device__ inline size_t reg_smem_doubles(int w, int LD, int cs) {
+    return static_cast<size_t>(w) * LD + 2 * cs * kMsg + static_cast<size_t>(cs) * KB * ns_max(w, cs) +
+           static_cast<size_t>(KB) * (KB + w) + part_elems(w) + KB * KB + 3 * KB + 4 + 4;
+}
+
+__device__ __forceinline__ RegSmem carve(double* sm, int w, int LD, int CS) {
+    RegSmem S;
+    S.chunk = sm;
+    S.msg = S.chunk + static_cast<size_t>(w) * LD;
+    S.rsb = S.msg + 2 * CS * kMsg;
+    S.zg = S.rsb + static_cast<size_t>(CS) * KB * ns_max(w, CS);
+    S.part = S.zg + static_cast<size_t>(KB) * (KB + w);
+    S.tmat = S.part + part_elems(w);
+    S.taus = S.tmat + KB * KB;
+    S.hsend = S.taus + KB;
+    S.wks = S.hsend + KB;
+    S.hs = S.wks + KB;
+    S.bar = reinterpret_cast<uint64_t*>(S.hs + 4);
+    return S;
+}
+
+__device__ __forceinline__ void dmma(double* c, double a0, double a1, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};\n"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a0), "d"(a1), "d"(b));
+}
+
+// Reflector entry V(li, c) of the micro-panel starting at global column j0:
+// unit lower trapezoidal (1 on the diagonal, 0 above, 0 for c >= kb).
+__device__ __forceinline__ double vent(const double* chunk, int LD, int li, int rc, int gi, int j0, int c, int kb) {
+    if (li >= rc || c >= kb) return 0.0;
+    const int j = j0 + c;
+    if (gi > j) return chunk[static_cast<size_t>(j) * LD + li];
+    return gi == j ? 1.0 : 0.0;
+}
+
+template <int MR>
+__global__ void __launch_bounds__(kT, 1)
+    hqr_reg_kernel(double* A, int64_t lda, int s, int w, int p, int R, int LD, double* tau, long long* trace) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = static_cast<int>(cluster.num_blocks());
+    const int rank = static_cast<int>(cluster.block_rank());
+    extern __shared__ __align__(16) double sm[];
+    const RegSmem S = carve(sm, w, LD, CS);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int r_beg = rank * R;
+    const int rc = max(0, min(s, r_beg + R) - r_beg);
+    const int nwact = max(1, min(kWarps, (rc + 31) >> 5));  // warps owning rows (warp 0 always)
+
+    for (int idx = tid; idx < w * rc; idx += kT) {
+        const int c = idx / rc, i = idx - c * rc;
+        S.chunk[static_cast<size_t>(c) * LD + i] = A[(r_beg + i) + static_cast<int64_t>(c) * lda];
+    }
+    // number of block phases: micro-panels with trailing columns beyond their register tile
+    int nphase = 0;
+    for (int j0 = 0; j0 < p; j0 += KB) nphase += (j0 + min(KB, w - j0) < w) ? 1 : 0;
+    const uint32_t col_bytes = static_cast<uint32_t>(CS * kMsg * 8);
+    auto rs_bytes = [&](int j0) {
+        const int kt = min(KB, w - j0), ncol = KB + w - j0 - kt, ns = (ncol + CS - 1) / CS;
+        const int mine = max(0, min(ncol, (rank + 1) * ns) - rank * ns);
+        return static_cast<uint32_t>(CS * KB * mine * 8);
+    };
+    auto ag_bytes = [&](int j0) {
+        const int kt = min(KB, w - j0);
+        return static_cast<uint32_t>(KB * (KB + w - j0 - kt) * 8);
+    };
+    auto next_phase_j0 = [&](int j0) {  // first micro-panel after j0 with a block phase, or -1
+        for (int jj = j0 + KB; jj < p; jj += KB)
+            if (jj + min(KB, w - jj) < w) return jj;
+        return -1;
+    };
+    if (tid == 0) {
+        for (int b = 0; b < 4; ++b) mbar_init(&S.bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (p > 0) mbar_arm(&S.bar[0], col_bytes);
+        if (p > 1) mbar_arm(&S.bar[1], col_bytes);
+        const int f = (0 + min(KB, w) < w && p > 0) ? 0 : next_phase_j0(0);
+        if (nphase > 0 && f >= 0) {
+            mbar_arm(&S.bar[2], rs_bytes(f));
+            mbar_arm(&S.bar[3], ag_bytes(f));
+        }
+    }
+    cluster.sync();  // every CTA live, barriers initialised, before any remote traffic
+
+    const uint32_t msg_a = smem_u32(S.msg);
+    const uint32_t bar0 = smem_u32(S.bar);  // mbarrier b at bar0 + 8 b
+
+    // Reduce the 16 per-thread partial dots over the CTA and all-gather them,
+    // with the head row of column jn, to every CTA's message slot jn & 1.
+    // Called by every thread (it contains the CTA barrier).
+    auto col_send = [&](double (&vals)[KB], int jn) {
+        if (warp < nwact) {
+            // butterfly reduce-scatter: after it lane l holds the sum of index l >> 1
+#pragma unroll
+            for (int lvl = 0; lvl < 4; ++lvl) {
+                const int o = 16 >> lvl, n = (KB / 2) >> lvl;
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < n; ++i) {
+                    const double send = up ? vals[i] : vals[i + n];
+                    const double keep = up ? vals[i + n] : vals[i];
+                    vals[i] = keep + __shfl_xor_sync(kFull, send, o);
+                }
+            }
+            const double v = vals[0] + __shfl_xor_sync(kFull, vals[0], 1);
+            if ((lane & 1) == 0) S.part[warp * KB + (lane >> 1)] = v;
+        }
+        __syncthreads();
+        if (trace && tid == 0 && rank == 0 && jn < 64) trace[jn * 8 + 4] = clock64();
+        if (warp == 0) {
+            double val = 0.0;
+            if (lane < KB) {
+                for (int ww = 0; ww < nwact; ++ww) val += S.part[ww * KB + lane];
+            } else if (jn >= r_beg && jn < r_beg + rc) {
+                val = S.hsend[lane - KB];
+            }
+            const int par = jn & 1;
+            const uint32_t off = msg_a + static_cast<uint32_t>(((par * CS + rank) * kMsg + lane) * 8);
+            for (int dst = 0; dst < CS; ++dst) st_async_f64(mapa_u32(off, dst), val, mapa_u32(bar0 + 8 * par, dst));
+            if (trace && tid == 0 && rank == 0 && jn < 64) trace[jn * 8 + 5] = clock64();
+        }
+    };
+
+    double x[MR][KB];
+    int phase = 0;
+    for (int j0 = 0; j0 < p; j0 += KB) {
+        const int kb = min(KB, p - j0), kt = min(KB, w - j0);
+        // ---- load the micro-panel tile into registers.  The tile is a window
+        // that shifts left by one column per step: x[m][k] is always column
+        // j + k of the current step j, so the step body is the same code for
+        // every column (a runtime loop; a fully unrolled 16-column body
+        // overflows the instruction cache).
+#pragma unroll
+        for (int m = 0; m < MR; ++m) {
+            const int li = tid + kT * m;
+#pragma unroll
+            for (int k = 0; k < KB; ++k)
+                x[m][k] = (li < rc && k < kt) ? S.chunk[static_cast<size_t>(j0 + k) * LD + li] : 0.0;
+        }
+        // ---- partials of column j0: x_j0' x_{j0+k} over rows > j0, head row j0
+        {
+            double vals[KB];
+#pragma unroll
+            for (int k = 0; k < KB; ++k) vals[k] = 0.0;
+#pragma unroll
+            for (int m = 0; m < MR; ++m) {
+                const int li = tid + kT * m, gi = r_beg + li;
+                if (li < rc && gi > j0) {
+#pragma unroll
+                    for (int k = 0; k < KB; ++k) vals[k] += x[m][0] * x[m][k];
+                } else if (li < rc && gi == j0) {
+#pragma unroll
+                    for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
+                }
+            }
+            col_send(vals, j0);
+        }
+        // ---- column steps.  Warp 0 waits for the column's message, computes
+        // house() and the 15 w_k (lane k), and publishes them; the warps that
+        // own rows then apply the reflector and accumulate the next column's
+        // partials.  Warps without rows (chunk shorter than the CTA) only
+        // take part in the barriers.
+#pragma unroll 1
+        for (int c = 0; c < kb; ++c) {
+            const int j = j0 + c, par = j & 1;
+            const bool tr = trace && tid == 0 && rank == 0 && j < 64;
+            if (tr) trace[j * 8 + 0] = clock64();
+            if (warp == 0) {
+                mbar_wait(&S.bar[par], static_cast<uint32_t>((j >> 1) & 1));
+                if (tr) trace[j * 8 + 1] = clock64();
+                double tsum = 0.0;
+                {
+                    const double* mp = S.msg + par * CS * kMsg + lane;
+                    for (int r = 0; r < CS; ++r) tsum += mp[r * kMsg];
+                }
+                // house() (householder.cpp:20-34)
+                const double sigma = __shfl_sync(kFull, tsum, 0);
+                const double alpha = __shfl_sync(kFull, tsum, KB);
+                const double hk = __shfl_sync(kFull, tsum, (lane + KB) & 31);  // lane k < 16: a(j, j+k)
+                double beta, tj, head = 1.0;
+                bool scale = false;
+                if (sigma == 0.0) {
+                    if (alpha >= 0.0) {
+                        beta = alpha;
+                        tj = 0.0;
+                    } else {
+                        beta = -alpha;
+                        tj = 2.0;
+                    }
+                } else {
+                    beta = sqrt(alpha * alpha + sigma);
+                    head = alpha >= 0.0 ? -sigma / (alpha + beta) : alpha - beta;
+                    tj = -head / beta;
+                    scale = true;
+                }
+                const double rh = 1.0 / head;
+                // w_k = tau (a(j,k) + sum_{i>j} v_i a(i,k)) = tau (h_k + d_k / head)
+                if (lane < KB) S.wks[lane] = tj * (hk + (scale ? tsum * rh : tsum));
+                if (lane == 0) {
+                    S.hs[0] = beta;
+                    S.hs[1] = scale ? rh : 1.0;
+                    S.hs[2] = tj;
+                    if (j + 2 < p) mbar_arm(&S.bar[par], col_bytes);
+                    if (rank == 0) tau[j] = tj;
+                    S.taus[c] = tj;
+                }
+            }
+            __syncthreads();
+            if (tr) trace[j * 8 + 2] = clock64();
+            const bool nxt = c + 1 < kb;
+            const int jn = j + 1;
+            double vals[KB];
+#pragma unroll
+            for (int k = 0; k < KB; ++k) vals[k] = 0.0;
+            if (warp < nwact) {
+                const double beta = S.hs[0], vs = S.hs[1], tj = S.hs[2];
+                // per-row multiplier of w_k: v_i below row j, 1 on row j, 0 above
+                double mult[MR], dm[MR];
+#pragma unroll
+                for (int m = 0; m < MR; ++m) {
+                    const int li = tid + kT * m, gi = r_beg + li;
+                    mult[m] = 0.0;
+                    if (li < rc && gi > j) {
+                        const double v = x[m][0] * vs;
+                        x[m][0] = v;
+                        mult[m] = v;
+                    } else if (li < rc && gi == j) {
+                        x[m][0] = beta;
+                        mult[m] = 1.0;
+                    }
+                    dm[m] = 0.0;
+                }
+                // apply the reflector to the window's live columns (householder.cpp:58-66)
+                // and accumulate the next column's partials x_{j+1}' a_k over rows > j+1
+                const int kr = kt - c - 1;  // live columns right of j in the window
+                if (tj != 0.0) {
+#pragma unroll
+                    for (int k = 1; k < KB; ++k) {
+                        if (k <= kr) {
+                            const double wk = S.wks[k];
+#pragma unroll
+                            for (int m = 0; m < MR; ++m) x[m][k] -= wk * mult[m];
+                        }
+                    }
+                }
+                if (nxt) {
+#pragma unroll
+                    for (int m = 0; m < MR; ++m) {
+                        const int li = tid + kT * m, gi = r_beg + li;
+                        dm[m] = (li < rc && gi > jn) ? x[m][1] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 1; k < KB; ++k) {
+                        if (k <= kr) {
+#pragma unroll
+                            for (int m = 0; m < MR; ++m) vals[k - 1] += dm[m] * x[m][k];
+                        }
+                    }
+                }
+                // retire column j to the chunk and shift the window
+#pragma unroll
+                for (int m = 0; m < MR; ++m) {
+                    const int li = tid + kT * m;
+                    if (li < rc) S.chunk[static_cast<size_t>(j) * LD + li] = x[m][0];
+#pragma unroll
+                    for (int k = 0; k + 1 < KB; ++k) x[m][k] = x[m][k + 1];
+                    x[m][KB - 1] = 0.0;
+                }
+                if (nxt) {
+#pragma unroll
+                    for (int m = 0; m < MR; ++m) {
+                        const int li = tid + kT * m, gi = r_beg + li;
+                        if (li < rc && gi == jn) {
+#pragma unroll
+                            for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
+                        }
+                    }
+                }
+            }
+            if (tr) trace[j * 8 + 3] = clock64();
+            if (nxt) col_send(vals, jn);
+        }
+        // ---- tile columns beyond the factorised ones (wide panels, p < w)
+#pragma unroll
+        for (int m = 0; m < MR; ++m) {
+            const int li = tid + kT * m;
+            if (li < rc) {
+#pragma unroll
+                for (int k = 0; k < KB; ++k)
+                    if (k < kt - kb) S.chunk[static_cast<size_t>(j0 + kb + k) * LD + li] = x[m][k];
+            }
+        }
+        __syncthreads();
+        if (j0 + kt >= w) continue;
+
+        // ---- block phase: A_t <- A_t - V T' (V' A_t), A_t = columns [j0 + kt, w)
+        const int nrest = w - j0 - kt, ncol = KB + nrest;
+        const int lo = min(rc, max(0, j0 - r_beg));  // local rows with gi >= j0
+        const int nk4 = (rc - lo + 3) >> 2;
+        {
+            // P = V'[V | A_t] over my rows: M = 16 (c), N = ncol (tiles of 8), K = rows
+            const int nt = (ncol + 7) >> 3;
+            const int ksplit = max(1, kWarps / nt);
+            for (int u = warp; u < nt * ksplit; u += kWarps) {
+                const int tile = u % nt, ks = u / nt;
+                const int kb0 = (ks * nk4) / ksplit, kb1 = ((ks + 1) * nk4) / ksplit;
+                const int q = tile * 8 + g;  // my B column
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int k4 = kb0; k4 < kb1; ++k4) {
+                    const int li = lo + 4 * k4 + t4, gi = r_beg + li;
+                    const double a0 = vent(S.chunk, LD, li, rc, gi, j0, g, kb);
+                    const double a1 = vent(S.chunk, LD, li, rc, gi, j0, g + 8, kb);
+                    double b;
+                    if (q < KB) b = vent(S.chunk, LD, li, rc, gi, j0, q, kb);
+                    else if (q < ncol && li < rc) b = S.chunk[static_cast<size_t>(j0 + kt + q - KB) * LD + li];
+                    else b = 0.0;
+                    dmma(acc, a0, a1, b);
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int row = g + (r >= 2 ? 8 : 0), col = tile * 8 + 2 * t4 + (r & 1);
+                    if (col < ncol) S.part[(static_cast<size_t>(ks) * KB + row) * ncol + col] = acc[r];
+                }
+            }
+            __syncthreads();
+            // reduce over the K splits (fixed order) and scatter column slices to their owners
+            const int ns = (ncol + CS - 1) / CS;
+            for (int e = tid; e < KB * ncol; e += kT) {
+                const int row = e / ncol, col = e - row * ncol;
+                double v = 0.0;
+                for (int ks = 0; ks < ksplit; ++ks) v += S.part[(static_cast<size_t>(ks) * KB + row) * ncol + col];
+                const int o = col / ns;
+                const uint32_t off =
+                    smem_u32(S.rsb + (static_cast<size_t>(rank) * KB + row) * ns + (col - o * ns));
+                st_async_f64(mapa_u32(off, o), v, mapa_u32(bar0 + 16, o));
+            }
+            // owner: sum the CS partial slices in rank order and broadcast
+            mbar_wait(&S.bar[2], static_cast<uint32_t>(phase & 1));
+            const int nxt = next_phase_j0(j0);
+            if (tid == 0 && nxt >= 0) mbar_arm(&S.bar[2], rs_bytes(nxt));
+            const int mine = max(0, min(ncol, (rank + 1) * ns) - rank * ns);
+            for (int e = tid; e < KB * mine; e += kT) {
+                const int row = e / mine, qq = e - row * mine;
+                double v = 0.0;
+                for (int src = 0; src < CS; ++src) v += S.rsb[(static_cast<size_t>(src) * KB + row) * ns + qq];
+                const uint32_t off = smem_u32(S.zg + static_cast<size_t>(row) * ncol + rank * ns + qq);
+                for (int dst = 0; dst < CS; ++dst) st_async_f64(mapa_u32(off, dst), v, mapa_u32(bar0 + 24, dst));
+            }
+            mbar_wait(&S.bar[3], static_cast<uint32_t>(phase & 1));
+            if (tid == 0 && nxt >= 0) mbar_arm(&S.bar[3], ag_bytes(nxt));
+            ++phase;
+        }
+        // T (form_wy_t recurrence, householder.cpp:69-97): T(c,c) = tau_c,
+        // T(0:c, c) = -tau_c T(0:c, 0:c) G(0:c, c), G = V'V = zg[:, 0:16]
+        if (warp == 0) {
+            double trow[KB];
+#pragma unroll
+            for (int c = 0; c < KB; ++c) {
+                const double tc = S.taus[c < kb ? c : 0];
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q < c; ++q) acc += trow[q] * S.zg[q * ncol + c];
+                trow[c] = c >= kb ? 0.0 : (lane < c ? -tc * acc : (lane == c ? tc : 0.0));
+            }
+            if (lane < KB)
+#pragma unroll
+                for (int c = 0; c < KB; ++c) S.tmat[lane * KB + c] = trow[c];
+        }
+        __syncthreads();
+        // Y = -T' Z in place (Z = zg[:, 16:])
+        for (int k = tid; k < nrest; k += kT) {
+            double z[KB];
+#pragma unroll
+            for (int q = 0; q < KB; ++q) z[q] = S.zg[q * ncol + KB + k];
+#pragma unroll
+            for (int c = 0; c < KB; ++c) {
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q <= c; ++q) acc += S.tmat[q * KB + c] * z[q];
+                S.zg[c * ncol + KB + k] = -acc;
+            }
+        }
+        __syncthreads();
+        // A_t += V Y over my rows >= j0: M = rows (tiles of 16), N = nrest (tiles of 8), K = 16
+        {
+            const int mt = (rc - lo + 15) >> 4, ntl = (nrest + 7) >> 3;
+            const int ngr = max(1, min(ntl, kWarps / max(1, mt)));
+            const int nk = (kb + 3) >> 2;
+            for (int u = warp; u < mt * ngr; u += kWarps) {
+                const int mi = u % mt, ng = u / mt;
+                const int r0 = lo + 16 * mi;
+                double av[4][2];
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int li = r0 + g + 8 * h;
+                        av[ks][h] = ks < nk ? vent(S.chunk, LD, li, rc, r_beg + li, j0, 4 * ks + t4, kb) : 0.0;
+                    }
+                for (int tn = ng; tn < ntl; tn += ngr) {
+                    const int colb = tn * 8;
+                    double acc[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
+                        acc[r] = (li < rc && col < nrest) ? S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li] : 0.0;
+                    }
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        if (ks < nk) {
+                            const int yc = colb + g;
+                            const double b = yc < nrest ? S.zg[(4 * ks + t4) * ncol + KB + yc] : 0.0;
+                            dmma(acc, av[ks][0], av[ks][1], b);
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
+                        if (li < rc && col < nrest) S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li] = acc[r];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    for (int idx = tid; idx < w * rc; idx += kT) {
+        const int c = idx / rc, i = idx - c * rc;
+        A[(r_beg + i) + static_cast<int64_t>(c) * lda] = S.chunk[static_cast<size_t>(c) * LD + i];
+    }
+    cluster.sync();  // no CTA exits while a peer may still write into it
+}
+
+int g_reg_cap = 0;  // dynamic shared memory cap for the kernel
+
+void reg_init() {
+    if (g_reg_cap) return;
+    g_reg_cap = dyn_smem_cap(reinterpret_cast<const void*>(hqr_reg_kernel<1>));
+    for (const void* f : {reinterpret_cast<const void*>(hqr_reg_kernel<1>),
+                          reinterpret_cast<const void*>(hqr_reg_kernel<2>)}) {
+        RUTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        RUTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, g_reg_cap));
+    }
+}
+
+}  // namespace
+
+// Largest column count the register kernel holds for s rows on cs CTAs (0 if
+// the chunk is too tall for 2 rows per thread).
+int qr_reg_capacity(int64_t s, int cs) {
+    reg_init();
+    const int64_t R = (s + cs - 1) / cs;
+    if (R > 2 * kT) return 0;
+    const int LD = static_cast<int>(R | 1);
+    int w = static_cast<int>((g_reg_cap - 512) / (8 * (LD + 4 * KB)));
+    while (w > 0 && reg_smem_doubles(w, LD, cs) * 8 > static_cast<size_t>(g_reg_cap) - 512) --w;
+    return std::max(w, 0);
+}
+
+// Rows per CTA the cluster size is chosen for (env RUTV_QR_ROWS, default 256).
+int qr_reg_rows() {
+    static int rows = [] {
+        const char* e = std::getenv("RUTV_QR_ROWS");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? v : 256;
+    }();
+    return rows;
+}
+
+void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
+    reg_init();
+    const int s = static_cast<int>(a.rows), w = static_cast<int>(a.cols);
+    const int p = std::min(s, w);
+    const int R = (s + cs - 1) / cs;
+    const int LD = R | 1;
+    const size_t smem = reg_smem_doubles(w, LD, cs) * 8;
+    if (smem > static_cast<size_t>(g_reg_cap) || R > 2 * kT)
+        throw Error(RUTV_ERR_INTERNAL, "hqr: sub-panel exceeds register-kernel capacity");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cs;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    static const bool tracing = std::getenv("RUTV_QR_TRACE") != nullptr;  // debug: per-column clock64 trace
+    long long* trace = nullptr;
+    if (tracing) {
+        RUTV_CUDA(cudaMalloc(&trace, 64 * 8 * sizeof(long long)));
+        RUTV_CUDA(cudaMemset(trace, 0, 64 * 8 * sizeof(long long)));
+    }
+    if (R <= kT)
+        RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<1>, a.data, a.ld, s, w, p, R, LD, tau, trace));
+    else
+        RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<2>, a.data, a.ld, s, w, p, R, LD, tau, trace));
+    note_launch();
+    if (tracing) {
+        long long h[64 * 8];
+        RUTV_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+        cudaFree(trace);
+        std::fprintf(stderr, "qr_reg trace s=%d w=%d cs=%d (cycles: wait, house, update, reduce, send, next)\n", s, w, cs);
+        for (int j = 0; j + 1 < std::min(p, 64); ++j) {
+            const long long* r = h + j * 8;
+            std::fprintf(stderr, "  col %2d: %6lld %6lld %6lld %6lld %6lld %6lld\n", j, r[1] - r[0], r[2] - r[1],
+                         r[3] - r[2], h[(j + 1) * 8 + 4] - r[3], h[(j + 1) * 8 + 5] - h[(j + 1) * 8 + 4],
+                         h[(j + 1) * 8 + 0] - h[(j + 1) * 8 + 5]);
+        }
+    }
+}
+
+}  // namespace rutv

@@ -97,7 +97,8 @@ def test_normal_fill_matches_host_stream():
 
 # ----------------------------------------------------------- Householder --
 @pytest.mark.parametrize("m,n", [(8, 5), (5, 5), (9, 2), (200, 16), (1000, 128), (4000, 128),
-                                 (3000, 256), (50, 64)])
+                                 (3000, 256), (50, 64), (37, 40), (300, 17), (513, 33), (2000, 128),
+                                 (10000, 64), (20000, 24)])
 def test_hqr_matches_oracle(m, n):
     a = _rand(m, n, 100 + m)
     qr_ref, tau_ref, twy_ref = oracle.hqr(a)
