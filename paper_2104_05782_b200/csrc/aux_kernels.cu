@@ -130,6 +130,123 @@ __global__ void __launch_bounds__(1024) form_t_kernel(const double* __restrict__
         }
 }
 
+
+// Twy by recursive doubling (p <= 256): the 16 x 16 diagonal blocks by the
+// reference recurrence (householder.cpp:84-95; one warp each, lane r holding
+// row r in registers), then block columns combined pairwise with doubling
+// width h = 16, 32, 64, ...:  T(I, J) = -T(I, I) (G(I, J) T(J, J)) -- the
+// compact-WY composition of two adjacent reflector blocks.  Every level is
+// two small triangular-times-dense products, 4 x 4 register tiles per thread.
+// M (G's strict upper triangle, overwritten by T) lives in shared memory for
+// p <= 128, else in the output buffer (L2-resident); the per-level scratch X
+// is in shared memory.
+constexpr int kFtThreads = 512;
+
+__global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __restrict__ gram, int64_t ldg,
+                                                               const double* __restrict__ tau, int p, double* t,
+                                                               int64_t ldt, int m_in_smem) {
+    extern __shared__ __align__(16) double fsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t LDm = m_in_smem ? p + 1 : ldt;
+    double* M = m_in_smem ? fsm : t;
+    double* X = fsm + (m_in_smem ? static_cast<size_t>(p) * (p + 1) : 0);
+    for (int i = tid; i < p * p; i += kFtThreads) {
+        const int r = i % p, c = i / p;
+        M[r + c * LDm] = r < c ? gram[r + c * ldg] : 0.0;
+    }
+    __syncthreads();
+    const int nb = (p + 15) >> 4;
+    for (int blk = warp; blk < nb; blk += kFtThreads / 32) {
+        const int I0 = blk * 16, bw = min(16, p - I0);
+        double trow[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const double tc = c < bw ? tau[I0 + c] : 0.0;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < c; ++q) {
+                const double gq = c < bw ? M[(I0 + q) + (I0 + c) * LDm] : 0.0;
+                if (q & 1) a1 += trow[q] * gq; else a0 += trow[q] * gq;
+            }
+            trow[c] = lane < c ? -tc * (a0 + a1) : (lane == c ? tc : 0.0);
+        }
+        __syncwarp();
+        if (lane < bw)
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < bw) M[(I0 + lane) + (I0 + c) * LDm] = trow[c];
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int h = 16; h < p; h *= 2) {
+        const int npair = (p + 2 * h - 1) / (2 * h);
+        const int tr = h >> 2;  // 4-row tiles per block
+        // X_pair = G(I, J) T(J, J), X_pair stored h x h at X + pair * h * h (column-major)
+        for (int e = tid; e < npair * tr * tr; e += kFtThreads) {
+            const int pr = e / (tr * tr), rem = e - pr * tr * tr;
+            const int ti = rem % tr, tj = rem / tr;
+            const int I0 = pr * 2 * h, J0 = I0 + h;
+            if (J0 >= p) continue;
+            const int hJ = min(h, p - J0);
+            const int r0 = 4 * ti, c0 = 4 * tj;
+            if (c0 >= hJ) continue;
+            double acc[4][4] = {};
+            const int lend = min(hJ, c0 + 4);
+            for (int l = 0; l < lend; ++l) {
+                double a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = M[(I0 + r0 + i) + (J0 + l) * LDm];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) b[jj] = c0 + jj < hJ ? M[(J0 + l) + (J0 + c0 + jj) * LDm] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] += a[i] * b[jj];
+            }
+            double* Xp = X + static_cast<size_t>(pr) * h * h;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) Xp[(r0 + i) + (c0 + jj) * h] = acc[i][jj];
+        }
+        __syncthreads();
+        // T(I, J) = -T(I, I) X_pair, T(I, I) upper triangular
+        for (int e = tid; e < npair * tr * tr; e += kFtThreads) {
+            const int pr = e / (tr * tr), rem = e - pr * tr * tr;
+            const int ti = rem % tr, tj = rem / tr;
+            const int I0 = pr * 2 * h, J0 = I0 + h;
+            if (J0 >= p) continue;
+            const int hJ = min(h, p - J0);
+            const int r0 = 4 * ti, c0 = 4 * tj;
+            if (c0 >= hJ) continue;
+            const double* Xp = X + static_cast<size_t>(pr) * h * h;
+            double acc[4][4] = {};
+            for (int m = r0; m < h; ++m) {
+                double a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = M[(I0 + r0 + i) + (I0 + m) * LDm];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) b[jj] = Xp[m + (c0 + jj) * h];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] += a[i] * b[jj];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (c0 + jj < hJ) M[(I0 + r0 + i) + (J0 + c0 + jj) * LDm] = -acc[i][jj];
+        }
+        __syncthreads();
+    }
+    if (m_in_smem)
+        for (int i = tid; i < p * p; i += kFtThreads) {
+            const int r = i % p, c = i / p;
+            t[r + c * ldt] = M[r + c * LDm];
+        }
+}
+
 }  // namespace
 
 void set_identity(cudaStream_t stream, const DView& a) {
@@ -176,6 +293,24 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
             double* t, int64_t ldt) {
     if (p == 0) return;
     if (p > 1024) throw Error(RUTV_ERR_NOTIMPL, "form_t: block size above 1024");
+    if (p <= 256) {
+        static int rcap = 0;
+        if (!rcap) {
+            rcap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_rd_kernel));
+            RUTV_CUDA(cudaFuncSetAttribute(form_t_rd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rcap));
+        }
+        // scratch X: npair h x h blocks per level
+        int64_t xe = 1;
+        for (int64_t h = 16; h < p; h *= 2) xe = std::max(xe, (p + 2 * h - 1) / (2 * h) * h * h);
+        const size_t xs = static_cast<size_t>(xe) * sizeof(double);
+        const size_t msz = static_cast<size_t>(p) * (p + 1) * sizeof(double);
+        const bool in_smem = msz + xs <= static_cast<size_t>(rcap);
+        form_t_rd_kernel<<<1, kFtThreads, in_smem ? msz + xs : xs, stream>>>(gram, ldg, tau, static_cast<int>(p), t,
+                                                                          ldt, in_smem ? 1 : 0);
+        note_launch();
+        RUTV_CHECK_LAUNCH();
+        return;
+    }
     static int cap = 0;
     if (!cap) {
         cap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_kernel));

@@ -63,8 +63,6 @@ struct RegSmem {
     double* tmat;   // [KB][KB] T, row-major
     double* taus;   // [KB]
     double* hsend;  // [KB] head row of the next column (row owner only)
-    double* wks;    // [KB] w_k of the current column (k = 1..15, window-relative)
-    double* hs;     // [4] beta, 1/head (or 1), tau
     uint64_t* bar;  // [4]: column parity 0/1, reduce-scatter, all-gather
 };
 
@@ -73,7 +71,7 @@ __host__ __device__ inline int part_elems(int w) { return KB * std::max(kWarps *
 
 __host__ __device__ inline size_t reg_smem_doubles(int w, int LD, int cs) {
     return static_cast<size_t>(w) * LD + 2 * cs * kMsg + static_cast<size_t>(cs) * KB * ns_max(w, cs) +
-           static_cast<size_t>(KB) * (KB + w) + part_elems(w) + KB * KB + 3 * KB + 4 + 4;
+           static_cast<size_t>(KB) * (KB + w) + part_elems(w) + KB * KB + 2 * KB + 4;
 }
 
 __device__ __forceinline__ RegSmem carve(double* sm, int w, int LD, int CS) {
@@ -86,9 +84,7 @@ __device__ __forceinline__ RegSmem carve(double* sm, int w, int LD, int CS) {
     S.tmat = S.part + part_elems(w);
     S.taus = S.tmat + KB * KB;
     S.hsend = S.taus + KB;
-    S.wks = S.hsend + KB;
-    S.hs = S.wks + KB;
-    S.bar = reinterpret_cast<uint64_t*>(S.hs + 4);
+    S.bar = reinterpret_cast<uint64_t*>(S.hsend + KB);
     return S;
 }
 
@@ -164,27 +160,25 @@ __global__ void __launch_bounds__(kT, 1)
     const uint32_t msg_a = smem_u32(S.msg);
     const uint32_t bar0 = smem_u32(S.bar);  // mbarrier b at bar0 + 8 b
 
-    // Reduce the 16 per-thread partial dots over the CTA and all-gather them,
-    // with the head row of column jn, to every CTA's message slot jn & 1.
-    // Called by every thread (it contains the CTA barrier).
+    // Reduce the 16 per-thread partial dots over the row-owning warps and
+    // all-gather them, with the head row of column jn, to every CTA's message
+    // slot jn & 1.  Called by the nwact row-owning warps only (named barrier).
     auto col_send = [&](double (&vals)[KB], int jn) {
-        if (warp < nwact) {
-            // butterfly reduce-scatter: after it lane l holds the sum of index l >> 1
+        // butterfly reduce-scatter: after it lane l holds the sum of index l >> 1
 #pragma unroll
-            for (int lvl = 0; lvl < 4; ++lvl) {
-                const int o = 16 >> lvl, n = (KB / 2) >> lvl;
-                const bool up = (lane & o) != 0;
+        for (int lvl = 0; lvl < 4; ++lvl) {
+            const int o = 16 >> lvl, n = (KB / 2) >> lvl;
+            const bool up = (lane & o) != 0;
 #pragma unroll
-                for (int i = 0; i < n; ++i) {
-                    const double send = up ? vals[i] : vals[i + n];
-                    const double keep = up ? vals[i + n] : vals[i];
-                    vals[i] = keep + __shfl_xor_sync(kFull, send, o);
-                }
+            for (int i = 0; i < n; ++i) {
+                const double send = up ? vals[i] : vals[i + n];
+                const double keep = up ? vals[i + n] : vals[i];
+                vals[i] = keep + __shfl_xor_sync(kFull, send, o);
             }
-            const double v = vals[0] + __shfl_xor_sync(kFull, vals[0], 1);
-            if ((lane & 1) == 0) S.part[warp * KB + (lane >> 1)] = v;
         }
-        __syncthreads();
+        const double v = vals[0] + __shfl_xor_sync(kFull, vals[0], 1);
+        if ((lane & 1) == 0) S.part[warp * KB + (lane >> 1)] = v;
+        asm volatile("bar.sync 1, %0;" ::"r"(nwact * 32) : "memory");
         if (trace && tid == 0 && rank == 0 && jn < 64) trace[jn * 8 + 4] = clock64();
         if (warp == 0) {
             double val = 0.0;
@@ -216,47 +210,52 @@ __global__ void __launch_bounds__(kT, 1)
             for (int k = 0; k < KB; ++k)
                 x[m][k] = (li < rc && k < kt) ? S.chunk[static_cast<size_t>(j0 + k) * LD + li] : 0.0;
         }
-        // ---- partials of column j0: x_j0' x_{j0+k} over rows > j0, head row j0
-        {
-            double vals[KB];
+        // ---- column steps, row-owning warps only (no CTA-wide barrier).
+        // Every such warp waits for the column's message itself, sums the CS
+        // partials in rank order and evaluates house() redundantly (identical
+        // in every warp of the cluster), lane k forming w_k.
+        if (warp < nwact) {
+            {  // partials of column j0: x_j0' x_{j0+k} over rows > j0, head row j0
+                double vals[KB];
 #pragma unroll
-            for (int k = 0; k < KB; ++k) vals[k] = 0.0;
+                for (int k = 0; k < KB; ++k) vals[k] = 0.0;
 #pragma unroll
-            for (int m = 0; m < MR; ++m) {
-                const int li = tid + kT * m, gi = r_beg + li;
-                if (li < rc && gi > j0) {
+                for (int m = 0; m < MR; ++m) {
+                    const int li = tid + kT * m, gi = r_beg + li;
+                    if (li < rc && gi > j0) {
 #pragma unroll
-                    for (int k = 0; k < KB; ++k) vals[k] += x[m][0] * x[m][k];
-                } else if (li < rc && gi == j0) {
+                        for (int k = 0; k < KB; ++k) vals[k] += x[m][0] * x[m][k];
+                    } else if (li < rc && gi == j0) {
 #pragma unroll
-                    for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
+                        for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
+                    }
                 }
+                col_send(vals, j0);
             }
-            col_send(vals, j0);
-        }
-        // ---- column steps.  Warp 0 waits for the column's message, computes
-        // house() and the 15 w_k (lane k), and publishes them; the warps that
-        // own rows then apply the reflector and accumulate the next column's
-        // partials.  Warps without rows (chunk shorter than the CTA) only
-        // take part in the barriers.
 #pragma unroll 1
-        for (int c = 0; c < kb; ++c) {
-            const int j = j0 + c, par = j & 1;
-            const bool tr = trace && tid == 0 && rank == 0 && j < 64;
-            if (tr) trace[j * 8 + 0] = clock64();
-            if (warp == 0) {
+            for (int c = 0; c < kb; ++c) {
+                const int j = j0 + c, par = j & 1;
+                const bool tr = trace && tid == 0 && rank == 0 && j < 64;
+                if (tr) trace[j * 8 + 0] = clock64();
                 mbar_wait(&S.bar[par], static_cast<uint32_t>((j >> 1) & 1));
                 if (tr) trace[j * 8 + 1] = clock64();
-                double tsum = 0.0;
+                double tsum;
                 {
                     const double* mp = S.msg + par * CS * kMsg + lane;
-                    for (int r = 0; r < CS; ++r) tsum += mp[r * kMsg];
+                    double t0 = 0.0, t1 = 0.0;
+                    int r = 0;
+                    for (; r + 1 < CS; r += 2) {
+                        t0 += mp[r * kMsg];
+                        t1 += mp[(r + 1) * kMsg];
+                    }
+                    if (r < CS) t0 += mp[r * kMsg];
+                    tsum = t0 + t1;
                 }
-                // house() (householder.cpp:20-34)
+                // house() (householder.cpp:20-34); 1/head and 1/beta by reciprocals
                 const double sigma = __shfl_sync(kFull, tsum, 0);
                 const double alpha = __shfl_sync(kFull, tsum, KB);
                 const double hk = __shfl_sync(kFull, tsum, (lane + KB) & 31);  // lane k < 16: a(j, j+k)
-                double beta, tj, head = 1.0;
+                double beta, tj, rh = 1.0;
                 bool scale = false;
                 if (sigma == 0.0) {
                     if (alpha >= 0.0) {
@@ -267,75 +266,59 @@ __global__ void __launch_bounds__(kT, 1)
                         tj = 2.0;
                     }
                 } else {
+                    const double rsig = __drcp_rn(sigma);
                     beta = sqrt(alpha * alpha + sigma);
-                    head = alpha >= 0.0 ? -sigma / (alpha + beta) : alpha - beta;
-                    tj = -head / beta;
+                    const double ab = alpha + beta;
+                    const double rbeta = __drcp_rn(beta);
+                    double head;
+                    if (alpha >= 0.0) {
+                        head = -sigma * __drcp_rn(ab);
+                        rh = -ab * rsig;
+                    } else {
+                        head = alpha - beta;
+                        rh = __drcp_rn(head);
+                    }
+                    tj = -head * rbeta;
                     scale = true;
                 }
-                const double rh = 1.0 / head;
-                // w_k = tau (a(j,k) + sum_{i>j} v_i a(i,k)) = tau (h_k + d_k / head)
-                if (lane < KB) S.wks[lane] = tj * (hk + (scale ? tsum * rh : tsum));
-                if (lane == 0) {
-                    S.hs[0] = beta;
-                    S.hs[1] = scale ? rh : 1.0;
-                    S.hs[2] = tj;
-                    if (j + 2 < p) mbar_arm(&S.bar[par], col_bytes);
-                    if (rank == 0) tau[j] = tj;
-                    S.taus[c] = tj;
-                }
-            }
-            __syncthreads();
-            if (tr) trace[j * 8 + 2] = clock64();
-            const bool nxt = c + 1 < kb;
-            const int jn = j + 1;
-            double vals[KB];
-#pragma unroll
-            for (int k = 0; k < KB; ++k) vals[k] = 0.0;
-            if (warp < nwact) {
-                const double beta = S.hs[0], vs = S.hs[1], tj = S.hs[2];
-                // per-row multiplier of w_k: v_i below row j, 1 on row j, 0 above
+                // lane k: w_k = tau (a(j,k) + sum_{i>j} v_i a(i,k)) = tau (h_k + d_k / head)
+                const double wkl = tj * (hk + (scale ? tsum * rh : tsum));
+                if (tr) trace[j * 8 + 2] = clock64();
+                // per-row multiplier of w_k: v_i below row j, 1 on row j, 0 above.
+                // Branch-free: padded window columns are zero and get w_k = 0, so
+                // every column of the window is updated unconditionally.
                 double mult[MR], dm[MR];
 #pragma unroll
                 for (int m = 0; m < MR; ++m) {
                     const int li = tid + kT * m, gi = r_beg + li;
-                    mult[m] = 0.0;
-                    if (li < rc && gi > j) {
-                        const double v = x[m][0] * vs;
-                        x[m][0] = v;
-                        mult[m] = v;
-                    } else if (li < rc && gi == j) {
-                        x[m][0] = beta;
-                        mult[m] = 1.0;
-                    }
-                    dm[m] = 0.0;
+                    const bool below = li < rc && gi > j, diag = li < rc && gi == j;
+                    const double v = scale ? x[m][0] * rh : x[m][0];
+                    mult[m] = below ? v : (diag ? 1.0 : 0.0);
+                    x[m][0] = below ? v : (diag ? beta : x[m][0]);
                 }
-                // apply the reflector to the window's live columns (householder.cpp:58-66)
-                // and accumulate the next column's partials x_{j+1}' a_k over rows > j+1
-                const int kr = kt - c - 1;  // live columns right of j in the window
-                if (tj != 0.0) {
+                // apply the reflector to the window (householder.cpp:58-66) and
+                // accumulate the next column's partials x_{j+1}' a_k over rows > j+1
+                const bool nxt = c + 1 < kb;
+                const int jn = j + 1;
 #pragma unroll
-                    for (int k = 1; k < KB; ++k) {
-                        if (k <= kr) {
-                            const double wk = S.wks[k];
+                for (int k = 1; k < KB; ++k) {
+                    const double wk = __shfl_sync(kFull, wkl, k);
 #pragma unroll
-                            for (int m = 0; m < MR; ++m) x[m][k] -= wk * mult[m];
-                        }
-                    }
+                    for (int m = 0; m < MR; ++m) x[m][k] -= wk * mult[m];
                 }
-                if (nxt) {
 #pragma unroll
-                    for (int m = 0; m < MR; ++m) {
-                        const int li = tid + kT * m, gi = r_beg + li;
-                        dm[m] = (li < rc && gi > jn) ? x[m][1] : 0.0;
-                    }
-#pragma unroll
-                    for (int k = 1; k < KB; ++k) {
-                        if (k <= kr) {
-#pragma unroll
-                            for (int m = 0; m < MR; ++m) vals[k - 1] += dm[m] * x[m][k];
-                        }
-                    }
+                for (int m = 0; m < MR; ++m) {
+                    const int li = tid + kT * m, gi = r_beg + li;
+                    dm[m] = (li < rc && gi > jn) ? x[m][1] : 0.0;
                 }
+                double vals[KB];
+#pragma unroll
+                for (int k = 0; k + 1 < KB; ++k) {
+                    vals[k] = 0.0;
+#pragma unroll
+                    for (int m = 0; m < MR; ++m) vals[k] += dm[m] * x[m][k + 1];
+                }
+                vals[KB - 1] = 0.0;
                 // retire column j to the chunk and shift the window
 #pragma unroll
                 for (int m = 0; m < MR; ++m) {
@@ -345,6 +328,12 @@ __global__ void __launch_bounds__(kT, 1)
                     for (int k = 0; k + 1 < KB; ++k) x[m][k] = x[m][k + 1];
                     x[m][KB - 1] = 0.0;
                 }
+                if (tid == 0) {  // off the critical chain: re-arm slot par, record tau
+                    if (j + 2 < p) mbar_arm(&S.bar[par], col_bytes);
+                    if (rank == 0) tau[j] = tj;
+                    S.taus[c] = tj;
+                }
+                if (tr) trace[j * 8 + 3] = clock64();
                 if (nxt) {
 #pragma unroll
                     for (int m = 0; m < MR; ++m) {
@@ -354,10 +343,9 @@ __global__ void __launch_bounds__(kT, 1)
                             for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
                         }
                     }
+                    col_send(vals, jn);
                 }
             }
-            if (tr) trace[j * 8 + 3] = clock64();
-            if (nxt) col_send(vals, jn);
         }
         // ---- tile columns beyond the factorised ones (wide panels, p < w)
 #pragma unroll
