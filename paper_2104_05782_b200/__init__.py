@@ -192,7 +192,7 @@ def factorize(a, *, b: int = 0, q: int = 1, algo: str = "b200", seed: int = 0,
 
 def factorize_device(a, t, u=None, v=None, *, b: int = 128, q: int = 1, seed: int = 0,
                      g=None, device: int | None = None, max_steps: int = -1,
-                     stream: int = 0) -> None:
+                     stream: int = 0, qr_prepass: bool = False) -> None:
     """Device-resident variant on torch CUDA tensors (column-major = a
     transposed contiguous row-major tensor; pass ``x.T`` views with stride (1, ld))."""
     def info(x):
@@ -203,7 +203,7 @@ def factorize_device(a, t, u=None, v=None, *, b: int = 128, q: int = 1, seed: in
     m, n = a.shape
     dev = a.device.index if device is None else device
     o = make_opts(b=b, q=q, seed=seed, build_u=u is not None, build_v=v is not None, device=dev,
-                  max_steps=max_steps, stream=stream)
+                  max_steps=max_steps, stream=stream, qr_prepass=qr_prepass)
     pa, lda = info(a)
     pt, ldt = info(t)
     pu, ldu = info(u)

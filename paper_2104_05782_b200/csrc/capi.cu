@@ -110,18 +110,23 @@ void run_factorize(const rutv_opts* o, const double* dA, int64_t m, int64_t n, i
                    const double* dG, int64_t g_len, double* dT, int64_t ldt, double* dU, int64_t ldu,
                    double* dV, int64_t ldv, cudaStream_t st) {
     check_opts(o);
-    if (m != n) throw Error(RUTV_ERR_NOTIMPL, "B200 path currently factors square matrices only");
-    if (o->qr_prepass && m > n) throw Error(RUTV_ERR_NOTIMPL, "qr_prepass not implemented");
+    const bool prepass = o->qr_prepass && m > n;
     if (lda < std::max<int64_t>(m, 1) || ldt < std::max<int64_t>(m, 1))
         throw Error(RUTV_ERR_SHAPE, "leading dimension smaller than the row count");
     if (o->build_u && (!dU || ldu < std::max<int64_t>(m, 1))) throw Error(RUTV_ERR_SHAPE, "U buffer");
     if (o->build_v && (!dV || ldv < std::max<int64_t>(n, 1))) throw Error(RUTV_ERR_SHAPE, "V buffer");
-    if (dG && g_len < rutv_b200_stream_length(m, n, o->b))
+    // qr_prepass factors the n x n R with the same seed (randutv_blocked.cpp:88-96)
+    if (dG && g_len < (prepass ? rutv_b200_stream_length(n, n, o->b) : rutv_b200_stream_length(m, n, o->b)))
         throw Error(RUTV_ERR_SHAPE, "explicit G shorter than the stream the factorization draws");
     rutv::FactorArgs fa{o->b,  o->q, o->build_u != 0, o->build_v != 0, o->seed, o->max_steps, dA, lda,
                         dG,    dT,   ldt,             dU,             ldu,     dV,          ldv,
                         o->overlap != 0};
-    rutv::factorize_device(st, o->device, n, fa);
+    if (prepass)
+        rutv::factorize_prepass_device(st, o->device, m, n, fa);
+    else if (m != n)
+        rutv::factorize_rect_device(st, o->device, m, n, fa);
+    else
+        rutv::factorize_device(st, o->device, n, fa);
 }
 
 }  // namespace
@@ -186,7 +191,9 @@ int rutv_b200_factorize(const rutv_opts* o, const double* A, int64_t m, int64_t 
         DMem<double> dA(static_cast<size_t>(mm * nn), s.s), dT(static_cast<size_t>(mm * nn), s.s);
         DMem<double> dU(o->build_u ? static_cast<size_t>(mm * mm) : 1, s.s);
         DMem<double> dV(o->build_v ? static_cast<size_t>(nn * nn) : 1, s.s);
-        const int64_t glen = G ? rutv_b200_stream_length(m, n, o->b) : 0;
+        const bool prepass = o->qr_prepass && m > n;  // the inner n x n run draws the stream
+        const int64_t glen = G ? (prepass ? rutv_b200_stream_length(n, n, o->b) : rutv_b200_stream_length(m, n, o->b))
+                               : 0;
         DMem<double> dG(G ? static_cast<size_t>(std::max<int64_t>(glen, 1)) : 1, s.s);
         if (mm * nn > 0)
             RUTV_CUDA(cudaMemcpy2DAsync(dA.p, static_cast<size_t>(mm) * 8, A, static_cast<size_t>(lda) * 8,

@@ -34,8 +34,14 @@ __global__ void scale_cols_kernel(int64_t rows, int64_t cols, double* a, int64_t
 // X (m x ncols) := leading ncols columns of Q = H_1 ... H_p from packed qr (m x p).
 void form_q(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
             double* scratch, int64_t scratch_elems) {
-    const int64_t m = qr.rows, ncols = x.cols;
     set_identity(st, x);
+    apply_q_left_blocked(st, qr, tau, p, x, scratch, scratch_elems);
+}
+
+void apply_q_left_blocked(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
+                          double* scratch, int64_t scratch_elems) {
+    const int64_t m = qr.rows, ncols = x.cols;
+    if (p == 0 || ncols == 0) return;
     const int64_t nb = 128;
     double* W = scratch;
     double* Gm = W + m * nb;

@@ -53,28 +53,6 @@ namespace {
 
 inline int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-// Stream-ordered device allocation from a pool that keeps its memory between
-// calls (cudaMallocAsync), so repeated factorizations do not pay cudaMalloc.
-struct DevBuf {
-    double* p = nullptr;
-    cudaStream_t st = nullptr;
-    DevBuf() = default;
-    DevBuf(int64_t elems, cudaStream_t s) : st(s) {
-        if (elems <= 0) elems = 1;
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(elems) * 8, s);
-        if (e == cudaErrorMemoryAllocation) {
-            cudaGetLastError();
-            throw Error(RUTV_ERR_OOM, "device allocation of " + std::to_string(elems * 8) + " bytes failed");
-        }
-        RUTV_CUDA(e);
-    }
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() {
-        if (p) cudaFreeAsync(p, st);
-    }
-};
-
 void configure_pool(int device) {
     static bool done[64] = {};
     if (device < 0 || device >= 64 || done[device]) return;

@@ -55,6 +55,28 @@ struct DView {
 
 enum class Op { N = 0, T = 1 };
 
+// Stream-ordered device allocation from the device's default pool
+// (cudaMallocAsync), so repeated calls do not pay cudaMalloc.
+struct DevBuf {
+    double* p = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf() = default;
+    DevBuf(int64_t elems, cudaStream_t s) : st(s) {
+        if (elems <= 0) elems = 1;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(elems) * 8, s);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            throw Error(RUTV_ERR_OOM, "device allocation of " + std::to_string(elems * 8) + " bytes failed");
+        }
+        if (e != cudaSuccess) throw Error(RUTV_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
 // Largest dynamic shared memory a kernel may request on this device, after its
 // static __shared__ usage (cudaDevAttrMaxSharedMemoryPerBlockOptin - static).
 inline int dyn_smem_cap(const void* kernel) {
@@ -159,6 +181,13 @@ struct FactorArgs {
     bool overlap = true;  // second stream for the off-critical-path work
 };
 void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& fa);
+// General m x n (rect.cu): the reference loop on one stream, rectangular
+// dense SVDs (svd_full) with orthonormal completion; qr_prepass for m > n.
+void factorize_rect_device(cudaStream_t st, int device, int64_t m, int64_t n, const FactorArgs& fa);
+void factorize_prepass_device(cudaStream_t st, int device, int64_t m, int64_t n, const FactorArgs& fa);
+// X <- Q X with Q = H_1...H_p from packed qr (householder.cpp:116-127, blocked).
+void apply_q_left_blocked(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
+                          double* scratch, int64_t scratch_elems);
 int last_profile(const char** names, double* ms, int cap);
 
 }  // namespace rutv
