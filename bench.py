@@ -273,10 +273,18 @@ def main():
         assert np.allclose(ht.numpy().T[:4, :4], t.cpu().numpy()[:4, :4])
 
     # ---- roofline of the dominant kernel (DMMA GEMM), separate profiled pass
+    # Streams serialized (RUTV_OVERLAP=0) so each GEMM's event bracket is its own
+    # launch time, not time shared with concurrent kernels of the other streams.
     os.environ["RUTV_GEMM_PROFILE"] = "1"
+    os.environ["RUTV_OVERLAP"] = "0"
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
     step()
+    p1.record(stream)
     torch.cuda.synchronize()
+    pass_ms = p0.elapsed_time(p1)
     os.environ["RUTV_GEMM_PROFILE"] = "0"
+    os.environ["RUTV_OVERLAP"] = "1"
     gp = rutv.gemm_profile()
     gemm_tflops = gp["flops"] / (gp["ms"] / 1e3) / 1e12 if gp["ms"] > 0 else None
     traffic = None
@@ -291,7 +299,8 @@ def main():
                 "frac": round(gemm_tflops / DMMA_PEAK_TFLOPS, 4) if gemm_tflops else None,
                 "traffic": traffic, "kernel": "dgemm_kernel (+split-K reduce)",
                 "gemm_ms_per_step": round(gp["ms"], 3), "gemm_launches": gp["launches"],
-                "gemm_share_of_step": round(gp["ms"] / ms, 4) if ms > 0 else None,
+                "gemm_share_of_serialized_step": round(gp["ms"] / pass_ms, 4) if pass_ms > 0 else None,
+                "serialized_step_ms": round(pass_ms, 3),
                 "step_frac_of_peak": round(F / (ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS, 4),
                 "peak_source": "measured DMMA burst (profiles/r01_dmma_peak.jsonl); "
                                "MEASURED_PEAKS.json has no FP64 entry"}
