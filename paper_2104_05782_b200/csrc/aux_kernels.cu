@@ -150,9 +150,32 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
     const int64_t LDm = m_in_smem ? p + 1 : ldt;
     double* M = m_in_smem ? fsm : t;
     double* X = fsm + (m_in_smem ? static_cast<size_t>(p) * (p + 1) : 0);
-    for (int i = tid; i < p * p; i += kFtThreads) {
-        const int r = i % p, c = i / p;
-        M[r + c * LDm] = r < c ? gram[r + c * ldg] : 0.0;
+    if (m_in_smem) {  // asynchronous copies: every load in flight at once
+        for (int i = tid; i < p * p; i += kFtThreads) {
+            const int r = i % p, c = i / p;
+            double* dst = M + r + c * LDm;
+            if (r < c) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gram + r + c * ldg));
+            } else {
+                *dst = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    } else {  // staged: 8 loads in flight per thread
+        for (int i0 = tid; i0 < p * p; i0 += 8 * kFtThreads) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * kFtThreads, r = i % p, c = i / p;
+                v[u] = (i < p * p && r < c) ? gram[r + c * ldg] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * kFtThreads;
+                if (i < p * p) M[i % p + (i / p) * LDm] = v[u];
+            }
+        }
     }
     __syncthreads();
     const int nb = (p + 15) >> 4;
@@ -188,14 +211,15 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
             const int I0 = pr * 2 * h, J0 = I0 + h;
             if (J0 >= p) continue;
             const int hJ = min(h, p - J0);
-            const int r0 = 4 * ti, c0 = 4 * tj;
+            const int r0 = ti, c0 = 4 * tj;  // rows ti + tr*i: lanes read consecutive rows
             if (c0 >= hJ) continue;
             double acc[4][4] = {};
             const int lend = min(hJ, c0 + 4);
+#pragma unroll 4
             for (int l = 0; l < lend; ++l) {
                 double a[4], b[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = M[(I0 + r0 + i) + (J0 + l) * LDm];
+                for (int i = 0; i < 4; ++i) a[i] = M[(I0 + r0 + tr * i) + (J0 + l) * LDm];
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) b[jj] = c0 + jj < hJ ? M[(J0 + l) + (J0 + c0 + jj) * LDm] : 0.0;
 #pragma unroll
@@ -207,7 +231,7 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) Xp[(r0 + i) + (c0 + jj) * h] = acc[i][jj];
+                for (int jj = 0; jj < 4; ++jj) Xp[(r0 + tr * i) + (c0 + jj) * h] = acc[i][jj];
         }
         __syncthreads();
         // T(I, J) = -T(I, I) X_pair, T(I, I) upper triangular
@@ -217,14 +241,15 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
             const int I0 = pr * 2 * h, J0 = I0 + h;
             if (J0 >= p) continue;
             const int hJ = min(h, p - J0);
-            const int r0 = 4 * ti, c0 = 4 * tj;
+            const int r0 = ti, c0 = 4 * tj;  // rows ti + tr*i (T(I,I) is zero left of each row's diagonal)
             if (c0 >= hJ) continue;
             const double* Xp = X + static_cast<size_t>(pr) * h * h;
             double acc[4][4] = {};
+#pragma unroll 4
             for (int m = r0; m < h; ++m) {
                 double a[4], b[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = M[(I0 + r0 + i) + (I0 + m) * LDm];
+                for (int i = 0; i < 4; ++i) a[i] = M[(I0 + r0 + tr * i) + (I0 + m) * LDm];
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) b[jj] = Xp[m + (c0 + jj) * h];
 #pragma unroll
@@ -236,7 +261,7 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj)
-                    if (c0 + jj < hJ) M[(I0 + r0 + i) + (J0 + c0 + jj) * LDm] = -acc[i][jj];
+                    if (c0 + jj < hJ) M[(I0 + r0 + tr * i) + (J0 + c0 + jj) * LDm] = -acc[i][jj];
         }
         __syncthreads();
     }
