@@ -24,9 +24,12 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cfloat>
 #include <vector>
 
+#include "cluster_msg.cuh"
 #include "rutv_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -59,9 +62,13 @@ __device__ __forceinline__ void rr_pair(int N, int r, int pi, int& p, int& q) {
     q = max(x, y);
 }
 
-template <int RPL>
+__device__ long long* g_jtrace = nullptr;  // debug: RUTV_JAC_TRACE per-round clock64 of CTA 0
+
+template <int RPL, bool VSM>
 __global__ void __launch_bounds__(kJThreads, 1)
-    jacobi_kernel(const SvdDesc* __restrict__ descs, int R, int vsm, int rs, double tol, int max_sweeps) {
+    jacobi_kernel(const SvdDesc* __restrict__ descs, int R, int vsm_unused, int rs, double tol, int max_sweeps) {
+    constexpr bool vsm = VSM;  // V in shared memory: compile-time, so V accesses are LDS / STS
+    (void)vsm_unused;
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = static_cast<int>(cluster.num_blocks());
     const int rank = static_cast<int>(cluster.block_rank());
@@ -71,11 +78,12 @@ __global__ void __launch_bounds__(kJThreads, 1)
     const int grp = lane / kLPP, sl = lane % kLPP;
     const int r_beg = rank * R;
     const int r_cnt = max(0, min(n, r_beg + R) - r_beg);
+    const int LB = R | 1;  // column stride of B / V: odd -> the 4 pair groups of a warp hit distinct banks
 
     extern __shared__ __align__(16) double sm[];
     double* Bs = sm;  // n columns x R rows
-    double* Vs = vsm ? Bs + static_cast<size_t>(n) * R : d.work + static_cast<size_t>(rank) * n * R;
-    double* xb = (vsm ? Vs : Bs) + static_cast<size_t>(n) * R;  // [2][CS][npairs][3]
+    double* Vs = vsm ? Bs + static_cast<size_t>(n) * LB : d.work + static_cast<size_t>(rank) * n * LB;
+    double* xb = (vsm ? Vs : Bs) + static_cast<size_t>(n) * LB;  // [2][CS][npairs][3]
     const size_t xpar = static_cast<size_t>(CS) * npairs * 3;
     __shared__ int s_rot;
     __shared__ double s_red[32];
@@ -86,8 +94,8 @@ __global__ void __launch_bounds__(kJThreads, 1)
         for (int i = tid; i < R; i += kJThreads) {
             double v = 0.0;
             if (i < r_cnt) v = d.A[(r_beg + i) + static_cast<int64_t>(c) * d.lda];
-            Bs[static_cast<size_t>(c) * R + i] = v;
-            Vs[static_cast<size_t>(c) * R + i] = (i < r_cnt && r_beg + i == c) ? 1.0 : 0.0;
+            Bs[static_cast<size_t>(c) * LB + i] = v;
+            Vs[static_cast<size_t>(c) * LB + i] = (i < r_cnt && r_beg + i == c) ? 1.0 : 0.0;
             fro += v * v;
         }
     fro = warp_sum(fro);
@@ -136,36 +144,71 @@ __global__ void __launch_bounds__(kJThreads, 1)
     // decides and broadcasts (c, s, flag) -- two barriers, O(npairs) words.
     const int slots = (npairs + CS - 1) / CS;
     double* dec = xb + static_cast<size_t>(CS) * slots * 3;  // rs mode: [npairs][3]
-    auto decide = [&](double al, double be, double ga, double& c, double& s, double& ratio) -> bool {
+    // all-gather mode: one mbarrier per round parity counts the peers' partials
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const uint32_t bar0 = smem_u32(s_bar);
+    const uint32_t xbytes = static_cast<uint32_t>((CS - 1) * npairs * 3 * 8);
+    int gr = 0;  // rounds done (both sweeps and check-only rounds)
+    if (!rs && CS > 1) {
+        if (tid == 0) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_arm(&s_bar[0], xbytes);
+            mbar_arm(&s_bar[1], xbytes);
+        }
+        cluster.sync();  // peers' barriers armed before any remote traffic
+    }
+    // zeta is formed before the skip tests (it only depends on the partials;
+    // unused -- possibly inf -- when the pair is skipped), so its division
+    // overlaps the two square roots; c = rsqrt(1 + t^2).
+    auto decide = [&](double al, double be, double ga, double& c, double& s, double& ratio, bool want_ratio) -> bool {
         const double np = sqrt(al), nq = sqrt(be);
+        const double zeta = (be - al) / (2.0 * ga);
         ratio = -1.0;
         if (np <= floor_col || nq <= floor_col) return false;
-        ratio = fabs(ga) / (np * nq);
-        if (fabs(ga) <= rel * np * nq) return false;
-        const double zeta = (be - al) / (2.0 * ga);
+        const double pq = np * nq;
+        if (want_ratio) ratio = fabs(ga) / pq;
+        if (fabs(ga) <= rel * pq) return false;
         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        c = 1.0 / sqrt(1.0 + tt * tt);
+        c = rsqrt(1.0 + tt * tt);
         s = c * tt;
         return true;
     };
     auto rotate = [&](int p, int q, double c, double s) {
-        double* bp = Bs + static_cast<size_t>(p) * R;
-        double* bq = Bs + static_cast<size_t>(q) * R;
-        double* vp = Vs + static_cast<size_t>(p) * R;
-        double* vq = Vs + static_cast<size_t>(q) * R;
+        double* bp = Bs + static_cast<size_t>(p) * LB;
+        double* bq = Bs + static_cast<size_t>(q) * LB;
+        double* vp = Vs + static_cast<size_t>(p) * LB;
+        double* vq = Vs + static_cast<size_t>(q) * LB;
+        // rows in chunks of 4: all loads of a chunk issue before its stores (the
+        // pointers may alias as far as the compiler knows)
 #pragma unroll
-        for (int t = 0; t < RPL; ++t) {
-            const int i = sl + kLPP * t;
-            if (i < r_cnt) {
-                const double x = bp[i], y = bq[i], vx = vp[i], vy = vq[i];
-                bp[i] = c * x - s * y;
-                bq[i] = s * x + c * y;
-                vp[i] = c * vx - s * vy;
-                vq[i] = s * vx + c * vy;
+        for (int t0 = 0; t0 < RPL; t0 += 4) {
+            double x[4], y[4], vx[4], vy[4];
+#pragma unroll
+            for (int u = 0; u < 4 && t0 + u < RPL; ++u) {
+                const int i = sl + kLPP * (t0 + u);
+                const bool ok = i < r_cnt;
+                x[u] = ok ? bp[i] : 0.0;
+                y[u] = ok ? bq[i] : 0.0;
+                vx[u] = ok ? vp[i] : 0.0;
+                vy[u] = ok ? vq[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4 && t0 + u < RPL; ++u) {
+                const int i = sl + kLPP * (t0 + u);
+                if (i < r_cnt) {
+                    bp[i] = c * x[u] - s * y[u];
+                    bq[i] = s * x[u] + c * y[u];
+                    vp[i] = c * vx[u] - s * vy[u];
+                    vq[i] = s * vx[u] + c * vy[u];
+                }
             }
         }
     };
+    long long* const jtr = (g_jtrace && blockIdx.x == 0 && tid == 0) ? g_jtrace : nullptr;
     auto round = [&](int r, int par, int mode, double& worst) -> bool {
+        if (jtr && gr < 64) jtr[gr * 4 + 0] = clock64();
         // phase 1: partial dots of every pair over my rows
         for (int base = 0; base < npairs; base += kPairsPerPass) {
             const int pi = base + warp * kPPW + grp;
@@ -174,8 +217,8 @@ __global__ void __launch_bounds__(kJThreads, 1)
             if (ok) rr_pair(N, r, pi, p, q);
             double a = 0.0, b = 0.0, g = 0.0;
             if (ok && q < n) {
-                const double* cp = Bs + static_cast<size_t>(p) * R;
-                const double* cq = Bs + static_cast<size_t>(q) * R;
+                const double* cp = Bs + static_cast<size_t>(p) * LB;
+                const double* cq = Bs + static_cast<size_t>(q) * LB;
 #pragma unroll
                 for (int t = 0; t < RPL; ++t) {
                     const int i = sl + kLPP * t;
@@ -202,24 +245,30 @@ __global__ void __launch_bounds__(kJThreads, 1)
                     slot[1] = b;
                     slot[2] = g;
                 }
-            } else if (CS == 1) {
-                if (sl == 0) {
-                    double* slot = xb + par * xpar + static_cast<size_t>(pi) * 3;
-                    slot[0] = a;
-                    slot[1] = b;
-                    slot[2] = g;
-                }
-            } else {
-                for (int dst = sl; dst < CS; dst += kLPP) {
-                    double* slot = cluster.map_shared_rank(xb, dst) + par * xpar +
-                                   (static_cast<size_t>(rank) * npairs + pi) * 3;
-                    slot[0] = a;
-                    slot[1] = b;
-                    slot[2] = g;
+            } else if (sl < 3) {
+                // lane sl owns value sl of the pair: written locally, and sent to
+                // every peer with st.async completing on its mbarrier `par`
+                const double val = sl == 0 ? a : (sl == 1 ? b : g);
+                double* slot = xb + par * xpar + (static_cast<size_t>(rank) * npairs + pi) * 3 + sl;
+                *slot = val;
+                if (CS > 1) {
+                    const uint32_t la = smem_u32(slot), lb = bar0 + 8 * par;
+                    for (int dst = 0; dst < CS; ++dst)
+                        if (dst != rank) st_async_f64(mapa_u32(la, dst), val, mapa_u32(lb, dst));
                 }
             }
         }
-        if (CS > 1) cluster.sync(); else __syncthreads();
+        if (rs) {
+            cluster.sync();
+        } else {
+            __syncthreads();  // local partials visible to the deciders
+            if (jtr && gr < 64) jtr[gr * 4 + 1] = clock64();
+            if (CS > 1 && tid < npairs) {
+                mbar_wait(&s_bar[par], static_cast<uint32_t>((gr >> 1) & 1));
+                if (tid == 0) mbar_arm(&s_bar[par], xbytes);  // round gr + 2
+            }
+            if (jtr && gr < 64) jtr[gr * 4 + 2] = clock64();
+        }
         bool any = false;
         if (rs) {
             // owners reduce their pairs in rank order and broadcast the decision
@@ -237,7 +286,7 @@ __global__ void __launch_bounds__(kJThreads, 1)
                         be += slot[1];
                         ga += slot[2];
                     }
-                    if (decide(al, be, ga, c, s, ratio) && mode == 0) flag = 1.0;
+                    if (decide(al, be, ga, c, s, ratio, mode == 1) && mode == 0) flag = 1.0;
                     if (mode == 1 && ratio >= 0.0) worst = fmax(worst, ratio);
                 }
                 for (int dst = 0; dst < CS; ++dst) {
@@ -260,31 +309,44 @@ __global__ void __launch_bounds__(kJThreads, 1)
                     rotate(p, q, dd[0], dd[1]);
                 }
         } else {
-            for (int base = 0; base < npairs; base += kPairsPerPass) {
-                const int pi = base + warp * kPPW + grp;
-                if (pi >= npairs) continue;
+            // one thread per pair decides (sums the CS partials in rank order:
+            // bit-identical decisions in every CTA), the 8-lane groups rotate
+            double* decl = xb + 2 * xpar;  // [npairs][3]
+            for (int pi = tid; pi < npairs; pi += kJThreads) {
                 int p, q;
                 rr_pair(N, r, pi, p, q);
-                if (q >= n) continue;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int rr = 0; rr < CS; ++rr) {
-                    const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
-                    al += slot[0];
-                    be += slot[1];
-                    ga += slot[2];
+                double c = 1.0, s = 0.0, flag = 0.0, ratio = -1.0;
+                if (q < n) {
+                    double al = 0.0, be = 0.0, ga = 0.0;
+                    for (int rr = 0; rr < CS; ++rr) {
+                        const double* slot = xb + par * xpar + (static_cast<size_t>(rr) * npairs + pi) * 3;
+                        al += slot[0];
+                        be += slot[1];
+                        ga += slot[2];
+                    }
+                    if (decide(al, be, ga, c, s, ratio, mode == 1) && mode == 0) flag = 1.0;
+                    if (mode == 1 && ratio >= 0.0) worst = fmax(worst, ratio);
                 }
-                double c, s, ratio;
-                const bool rot = decide(al, be, ga, c, s, ratio);
-                if (mode == 1) {
-                    if (ratio >= 0.0) worst = fmax(worst, ratio);
-                    continue;
-                }
-                if (!rot) continue;
-                any = true;
-                rotate(p, q, c, s);
+                decl[3 * pi] = c;
+                decl[3 * pi + 1] = s;
+                decl[3 * pi + 2] = flag;
             }
+            __syncthreads();
+            if (mode == 0)
+                for (int base = 0; base < npairs; base += kPairsPerPass) {
+                    const int pi = base + warp * kPPW + grp;
+                    if (pi >= npairs) continue;
+                    const double* dd = decl + 3 * pi;
+                    if (dd[2] == 0.0) continue;
+                    int p, q;
+                    rr_pair(N, r, pi, p, q);
+                    any = true;
+                    rotate(p, q, dd[0], dd[1]);
+                }
         }
+        if (jtr && gr < 64) jtr[gr * 4 + 3] = clock64();
         __syncthreads();
+        ++gr;
         return any;
     };
 
@@ -329,7 +391,7 @@ __global__ void __launch_bounds__(kJThreads, 1)
     // sigma_j = ||b_j||: partial column sums, all-gathered, summed in rank order.
     if (CS > 1) cluster.sync();  // every CTA done reading xb
     for (int c = warp; c < n; c += nwarps) {
-        const double* cc = Bs + static_cast<size_t>(c) * R;
+        const double* cc = Bs + static_cast<size_t>(c) * LB;
         double a = 0.0;
         for (int i = lane; i < r_cnt; i += 32) a += cc[i] * cc[i];
         a = warp_sum(a);
@@ -362,9 +424,9 @@ __global__ void __launch_bounds__(kJThreads, 1)
         const double s = s_sig[j];
         for (int i = tid; i < r_cnt; i += kJThreads) {
             const int64_t row = r_beg + i;
-            d.V[row + static_cast<int64_t>(t) * n] = Vs[static_cast<size_t>(j) * R + i];
+            d.V[row + static_cast<int64_t>(t) * n] = Vs[static_cast<size_t>(j) * LB + i];
             d.U[row + static_cast<int64_t>(t) * n] =
-                s > floor_col ? Bs[static_cast<size_t>(j) * R + i] / s : 0.0;
+                s > floor_col ? Bs[static_cast<size_t>(j) * LB + i] / s : 0.0;
         }
     }
     if (rank == 0) {
@@ -390,7 +452,7 @@ __global__ void complete_kernel(const SvdDesc* __restrict__ descs) {
     const int kept = static_cast<int>(d.status[2]);
     if (d.status[0] != 0.0 || kept >= n) return;
     double* U = d.U;
-    double* cand = d.work + static_cast<size_t>(n) * n;
+    double* cand = d.work + static_cast<size_t>(n) * (n + 16);
     __shared__ double red[32];
     __shared__ double s_val;
     const int nw = blockDim.x >> 5;
@@ -438,20 +500,32 @@ struct JCfg {
 
 int g_jcap = 0, g_jmax_cluster = 0;
 
-template <int RPL>
+template <int RPL, bool VSM>
 void prep_kernel() {
-    auto k = jacobi_kernel<RPL>;
+    auto k = jacobi_kernel<RPL, VSM>;
     RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, g_jcap));
 }
 
+template <int RPL>
+void launch_j(cudaLaunchConfig_t& cfg, int vsm, const SvdDesc* d, int R, int rs, double tol, int max_sweeps) {
+    if (vsm)
+        RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<RPL, true>, d, R, vsm, rs, tol, max_sweeps));
+    else
+        RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<RPL, false>, d, R, vsm, rs, tol, max_sweeps));
+}
+
 void jinit() {
     if (g_jcap) return;
-    g_jcap = dyn_smem_cap(reinterpret_cast<const void*>(jacobi_kernel<16>));
-    prep_kernel<2>();
-    prep_kernel<4>();
-    prep_kernel<8>();
-    prep_kernel<16>();
+    g_jcap = dyn_smem_cap(reinterpret_cast<const void*>(jacobi_kernel<16, true>));
+    prep_kernel<2, true>();
+    prep_kernel<4, true>();
+    prep_kernel<8, true>();
+    prep_kernel<16, true>();
+    prep_kernel<2, false>();
+    prep_kernel<4, false>();
+    prep_kernel<8, false>();
+    prep_kernel<16, false>();
     g_jmax_cluster = 8;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16);
@@ -465,7 +539,7 @@ void jinit() {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, jacobi_kernel<16>, &cfg) == cudaSuccess && ncl > 0)
+    if (cudaOccupancyMaxActiveClusters(&ncl, jacobi_kernel<16, true>, &cfg) == cudaSuccess && ncl > 0)
         g_jmax_cluster = 16;
     cudaGetLastError();
 }
@@ -476,16 +550,20 @@ size_t jsmem_bytes(int n, int R, int cs, bool vsm) {
     const int npairs = (n + (n & 1)) / 2;
     const size_t slots = (static_cast<size_t>(npairs) + cs - 1) / cs;
     const size_t xg = use_rs(n, cs) ? static_cast<size_t>(cs) * slots * 3 + 3 * static_cast<size_t>(npairs)
-                                    : 2 * static_cast<size_t>(cs) * npairs * 3;
+                                    : 2 * static_cast<size_t>(cs) * npairs * 3 + 3 * static_cast<size_t>(npairs);
     const size_t x = std::max<size_t>(xg, static_cast<size_t>(cs) * n + 8);
-    return (static_cast<size_t>(n) * R * (vsm ? 2 : 1) + x) * sizeof(double);
+    return (static_cast<size_t>(n) * (R | 1) * (vsm ? 2 : 1) + x) * sizeof(double);
 }
 
-JCfg choose(int n) {
+JCfg choose(int n, int count = 1) {
     jinit();
     const size_t cap = static_cast<size_t>(g_jcap) - 512;
     JCfg c{1, std::max(n, 1), 1, 16, 0};
-    for (int cs = 1;; cs *= 2) {
+    static const int force_cs = [] {  // tuning knob: RUTV_JACOBI_CS=k starts the search at k CTAs
+        const char* e = std::getenv("RUTV_JACOBI_CS");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    for (int cs = force_cs;; cs *= 2) {
         const int R = std::max(1, (n + cs - 1) / cs);
         if (R <= kLPP * 16 && jsmem_bytes(n, R, cs, true) <= cap) {
             c = {cs, R, 1, 0, jsmem_bytes(n, R, cs, true)};
@@ -499,6 +577,14 @@ JCfg choose(int n) {
             break;
         }
     }
+    // Each round streams the CTA's rows of B and V through shared memory, so
+    // time per round scales with the rows per CTA: spread a problem over more
+    // CTAs while the whole batch still fits in one wave of SMs.
+    while (c.vsm && c.cs * 2 <= g_jmax_cluster && static_cast<int64_t>(count) * c.cs * 2 <= kNumSMs &&
+           (n + 2 * c.cs - 1) / (2 * c.cs) >= 16 && !use_rs(n, c.cs * 2)) {
+        const int cs = c.cs * 2, R = (n + cs - 1) / cs;
+        c = {cs, R, 1, 0, jsmem_bytes(n, R, cs, true)};
+    }
     const int rpl = (c.R + kLPP - 1) / kLPP;
     c.rpl = rpl <= 2 ? 2 : rpl <= 4 ? 4 : rpl <= 8 ? 8 : 16;
     return c;
@@ -506,12 +592,13 @@ JCfg choose(int n) {
 
 }  // namespace
 
-int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) { return n * n + n + 64; }
+// V spill (CS x n x (R | 1) <= n (n + 16)) + completion candidate
+int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) { return n * (n + 16) + n + 64; }
 
 void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol,
                int max_sweeps) {
     if (count <= 0) return;
-    const JCfg c = choose(nmax);
+    const JCfg c = choose(nmax, count);
     const int rs = use_rs(nmax, c.cs) ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(count * c.cs));
@@ -525,11 +612,35 @@ void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax,
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
+    static const bool jtrace = std::getenv("RUTV_JAC_TRACE") != nullptr;
+    long long* dtr = nullptr;
+    if (jtrace) {
+        RUTV_CUDA(cudaMalloc(&dtr, 64 * 4 * sizeof(long long)));
+        RUTV_CUDA(cudaMemset(dtr, 0, 64 * 4 * sizeof(long long)));
+        RUTV_CUDA(cudaMemcpyToSymbol(g_jtrace, &dtr, sizeof(dtr)));
+    }
+    struct TraceOut {
+        long long* p;
+        int cs;
+        ~TraceOut() {
+            if (!p) return;
+            long long h[256];
+            cudaDeviceSynchronize();
+            cudaMemcpy(h, p, sizeof(h), cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "jacobi trace cs=%d (cycles: dots+send, wait, decide+rotate, next)\n", cs);
+            for (int r = 0; r + 1 < 16; ++r)
+                std::fprintf(stderr, "  round %2d: %6lld %6lld %6lld %6lld\n", r, h[r * 4 + 1] - h[r * 4], h[r * 4 + 2] - h[r * 4 + 1],
+                             h[r * 4 + 3] - h[r * 4 + 2], h[(r + 1) * 4] - h[r * 4 + 3]);
+            long long* z = nullptr;
+            cudaMemcpyToSymbol(g_jtrace, &z, sizeof(z));
+            cudaFree(p);
+        }
+    } tro{dtr, c.cs};
     switch (c.rpl) {
-        case 2: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<2>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
-        case 4: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<4>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
-        case 8: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<8>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
-        default: RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel<16>, d_descs, c.R, c.vsm, rs, tol, max_sweeps)); break;
+        case 2: launch_j<2>(cfg, c.vsm, d_descs, c.R, rs, tol, max_sweeps); break;
+        case 4: launch_j<4>(cfg, c.vsm, d_descs, c.R, rs, tol, max_sweeps); break;
+        case 8: launch_j<8>(cfg, c.vsm, d_descs, c.R, rs, tol, max_sweeps); break;
+        default: launch_j<16>(cfg, c.vsm, d_descs, c.R, rs, tol, max_sweeps); break;
     }
     note_launch();
     complete_kernel<<<count, 256, 0, stream>>>(d_descs);
