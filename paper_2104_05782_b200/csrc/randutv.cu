@@ -336,8 +336,29 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
         svd_batch(st, reinterpret_cast<const SvdDesc*>(Ddesc.p), nsteps, static_cast<int>(nmax), 1e-15, 30);
         prof.mark(P_SVD);
         const cudaEvent_t evS = record(st);
+        // Products with the SVD factors: one grouped in-place launch per kind
+        // when the blocks fit the grouped kernel (w <= 128), else per-step GEMMs.
+        const bool grouped = bb <= small_mul_max_w();
+        int64_t ext_r = 0, ext_l = 0;
+        for (const StepInfo& si : plan) {
+            ext_r += vr + si.r0 + n;
+            ext_l += si.s;
+        }
+        const size_t gsb = small_mul_scratch_bytes(static_cast<size_t>(nsteps), std::max(ext_r, ext_l));
+        DevBuf GsA(static_cast<int64_t>(2 * gsb / 8 + 8), st), GsB(static_cast<int64_t>(gsb / 8 + 8), st);
+        DevBuf GsD(static_cast<int64_t>(nsteps * sizeof(RectDiagDesc) / 8 + 8), st);
         // U right-multiplies on stream B (disjoint buffer)
-        if (bu) {
+        if (bu && grouped) {
+            wait(sB, evS);
+            std::vector<SmallMulDesc> ud;
+            for (int i = 0; i < nsteps; ++i) {
+                const StepInfo& si = plan[static_cast<size_t>(i)];
+                const int64_t w = si.tail ? si.s : b;
+                ud.push_back({umat.data + si.r0 * umat.ld, umat.ld, n, w, Usall.p + static_cast<int64_t>(i) * bb * bb, w,
+                              static_cast<int>(w), 0});
+            }
+            small_mul_grouped(sB, false, ud, GsB.p, gsb);
+        } else if (bu) {
             wait(sB, evS);
             for (int i = 0; i < nsteps; ++i) {
                 const StepInfo& si = plan[static_cast<size_t>(i)];
@@ -351,29 +372,54 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
         }
         // diagonal writes (finished panel columns), then strips (row blocks),
         // then V/T right-multiplies (column blocks) on stream A
-        for (int i = 0; i < nsteps; ++i) {
-            const StepInfo& si = plan[static_cast<size_t>(i)];
-            const int64_t w = si.tail ? si.s : b;
-            write_rect_diag(st, tmat.block(si.r0, si.r0, si.s, w), Sall.p + static_cast<int64_t>(i) * (bb + 1), w);
+        {
+            std::vector<RectDiagDesc> rd;
+            for (int i = 0; i < nsteps; ++i) {
+                const StepInfo& si = plan[static_cast<size_t>(i)];
+                const int64_t w = si.tail ? si.s : b;
+                DView blk = tmat.block(si.r0, si.r0, si.s, w);
+                rd.push_back({blk.data, blk.rows, blk.cols, blk.ld, Sall.p + static_cast<int64_t>(i) * (bb + 1), w});
+            }
+            rect_diag_grouped(st, rd, GsD.p, static_cast<size_t>(nsteps) * sizeof(RectDiagDesc));
         }
-        for (int i = 0; i < nsteps; ++i) {
-            const StepInfo& si = plan[static_cast<size_t>(i)];
-            if (si.tail) continue;
-            const int64_t off = static_cast<int64_t>(i) * bb * bb;
-            DView strip = tmat.block(si.r0, si.r0 + b, b, si.s - b);
-            DView tmp(b, si.s - b, b, ZlA.p);
-            gemmA(1.0, Op::T, DView(b, b, b, Usall.p + off), Op::N, strip, 0.0, tmp);
-            copy_view(st, strip, tmp);
-        }
-        for (int i = 0; i < nsteps; ++i) {
-            const StepInfo& si = plan[static_cast<size_t>(i)];
-            const int64_t w = si.tail ? si.s : b;
-            if (vr + si.r0 == 0) continue;
-            const int64_t off = static_cast<int64_t>(i) * bb * bb;
-            DView X = vt.block(0, si.r0, vr + si.r0, w);
-            DView tmp(vr + si.r0, w, vr + si.r0, ZxA.p);
-            gemmA(1.0, Op::N, X, Op::N, DView(w, w, w, Vsall.p + off), 0.0, tmp);
-            copy_view(st, X, tmp);
+        if (grouped) {
+            std::vector<SmallMulDesc> sd, vd;
+            for (int i = 0; i < nsteps; ++i) {
+                const StepInfo& si = plan[static_cast<size_t>(i)];
+                const int64_t off = static_cast<int64_t>(i) * bb * bb;
+                const int64_t w = si.tail ? si.s : b;
+                if (!si.tail && si.s > b) {
+                    DView strip = tmat.block(si.r0, si.r0 + b, b, si.s - b);
+                    sd.push_back({strip.data, strip.ld, b, si.s - b, Usall.p + off, b, static_cast<int>(b), 0});
+                }
+                if (vr + si.r0 > 0) {
+                    DView X = vt.block(0, si.r0, vr + si.r0, w);
+                    vd.push_back({X.data, X.ld, vr + si.r0, w, Vsall.p + off, w, static_cast<int>(w), 0});
+                }
+            }
+            // strips (row blocks) strictly before the column-block right-multiplies
+            small_mul_grouped(st, true, sd, GsA.p, gsb);
+            small_mul_grouped(st, false, vd, reinterpret_cast<char*>(GsA.p) + gsb, gsb);
+        } else {
+            for (int i = 0; i < nsteps; ++i) {
+                const StepInfo& si = plan[static_cast<size_t>(i)];
+                if (si.tail) continue;
+                const int64_t off = static_cast<int64_t>(i) * bb * bb;
+                DView strip = tmat.block(si.r0, si.r0 + b, b, si.s - b);
+                DView tmp(b, si.s - b, b, ZlA.p);
+                gemmA(1.0, Op::T, DView(b, b, b, Usall.p + off), Op::N, strip, 0.0, tmp);
+                copy_view(st, strip, tmp);
+            }
+            for (int i = 0; i < nsteps; ++i) {
+                const StepInfo& si = plan[static_cast<size_t>(i)];
+                const int64_t w = si.tail ? si.s : b;
+                if (vr + si.r0 == 0) continue;
+                const int64_t off = static_cast<int64_t>(i) * bb * bb;
+                DView X = vt.block(0, si.r0, vr + si.r0, w);
+                DView tmp(vr + si.r0, w, vr + si.r0, ZxA.p);
+                gemmA(1.0, Op::N, X, Op::N, DView(w, w, w, Vsall.p + off), 0.0, tmp);
+                copy_view(st, X, tmp);
+            }
         }
         if (bu && overlap) wait(st, record(sB));
         prof.mark(P_BETA);

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/rutv_b200.h"
 
@@ -181,6 +182,30 @@ struct FactorArgs {
     bool overlap = true;  // second stream for the off-critical-path work
 };
 void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& fa);
+// grouped.cu: in-place X_i <- X_i M_i (right) or X_i <- M_i' X_i (left) for many
+// small square M_i (w <= small_mul_max_w()) in one launch.
+struct SmallMulDesc {
+    double* X;
+    int64_t ldx;
+    int64_t rows, cols;  // right: rows x w; left: w x cols
+    const double* M;
+    int64_t ldm;
+    int w;
+    int pad;
+};
+int small_mul_max_w();
+struct RectDiagDesc {
+    double* A;
+    int64_t rows, cols, ld;
+    const double* sigma;
+    int64_t p;
+};
+void rect_diag_grouped(cudaStream_t st, const std::vector<RectDiagDesc>& descs, void* dev_scratch,
+                       size_t scratch_bytes);
+void small_mul_grouped(cudaStream_t st, bool left, const std::vector<SmallMulDesc>& descs, void* dev_scratch,
+                       size_t scratch_bytes);
+size_t small_mul_scratch_bytes(size_t ndesc, int64_t total_extent);
+
 // General m x n (rect.cu): the reference loop on one stream, rectangular
 // dense SVDs (svd_full) with orthonormal completion; qr_prepass for m > n.
 void factorize_rect_device(cudaStream_t st, int device, int64_t m, int64_t n, const FactorArgs& fa);
