@@ -142,9 +142,13 @@ __global__ void __launch_bounds__(1024) form_t_kernel(const double* __restrict__
 // is in shared memory.
 constexpr int kFtThreads = 512;
 
+// mode 1: the same recursive doubling computes the inverse X of an upper
+// triangular R (input `gram` = R, diagonal included): diagonal blocks by back
+// substitution (the recurrence with tau_c -> 1 / R(c, c)), off-diagonal blocks
+// X(I, J) = -X(I, I) R(I, J) X(J, J).
 __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __restrict__ gram, int64_t ldg,
                                                                const double* __restrict__ tau, int p, double* t,
-                                                               int64_t ldt, int m_in_smem) {
+                                                               int64_t ldt, int m_in_smem, int mode) {
     extern __shared__ __align__(16) double fsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t LDm = m_in_smem ? p + 1 : ldt;
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
         for (int i = tid; i < p * p; i += kFtThreads) {
             const int r = i % p, c = i / p;
             double* dst = M + r + c * LDm;
-            if (r < c) {
+            if (r < c || (mode == 1 && r == c)) {
                 const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gram + r + c * ldg));
             } else {
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i = i0 + u * kFtThreads, r = i % p, c = i / p;
-                v[u] = (i < p * p && r < c) ? gram[r + c * ldg] : 0.0;
+                v[u] = (i < p * p && (r < c || (mode == 1 && r == c))) ? gram[r + c * ldg] : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(kFtThreads) form_t_rd_kernel(const double* __r
         double trow[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-            const double tc = c < bw ? tau[I0 + c] : 0.0;
+            const double tc = c >= bw ? 0.0 : (mode == 1 ? 1.0 / M[(I0 + c) + (I0 + c) * LDm] : tau[I0 + c]);
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
             for (int q = 0; q < c; ++q) {
@@ -331,7 +335,7 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
         const size_t msz = static_cast<size_t>(p) * (p + 1) * sizeof(double);
         const bool in_smem = msz + xs <= static_cast<size_t>(rcap);
         form_t_rd_kernel<<<1, kFtThreads, in_smem ? msz + xs : xs, stream>>>(gram, ldg, tau, static_cast<int>(p), t,
-                                                                          ldt, in_smem ? 1 : 0);
+                                                                          ldt, in_smem ? 1 : 0, 0);
         note_launch();
         RUTV_CHECK_LAUNCH();
         return;
@@ -347,6 +351,25 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
     if (!in_smem && xs > static_cast<size_t>(cap)) throw Error(RUTV_ERR_NOTIMPL, "form_t: block too large");
     form_t_kernel<<<1, 1024, in_smem ? tsm + xs : xs, stream>>>(gram, ldg, tau, static_cast<int>(p), t, ldt,
                                                                 in_smem ? 1 : 0);
+    note_launch();
+    RUTV_CHECK_LAUNCH();
+}
+
+void tri_inv_upper(cudaStream_t stream, const double* r, int64_t ldr, int64_t p, double* x, int64_t ldx) {
+    if (p == 0) return;
+    if (p > 256) throw Error(RUTV_ERR_NOTIMPL, "tri_inv_upper: order above 256");
+    static int rcap = 0;
+    if (!rcap) {
+        rcap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_rd_kernel));
+        RUTV_CUDA(cudaFuncSetAttribute(form_t_rd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rcap));
+    }
+    int64_t xe = 1;
+    for (int64_t h = 16; h < p; h *= 2) xe = std::max(xe, (p + 2 * h - 1) / (2 * h) * h * h);
+    const size_t xs = static_cast<size_t>(xe) * sizeof(double);
+    const size_t msz = static_cast<size_t>(p) * (p + 1) * sizeof(double);
+    const bool in_smem = msz + xs <= static_cast<size_t>(rcap);
+    form_t_rd_kernel<<<1, kFtThreads, in_smem ? msz + xs : xs, stream>>>(r, ldr, nullptr, static_cast<int>(p), x, ldx,
+                                                                      in_smem ? 1 : 0, 1);
     note_launch();
     RUTV_CHECK_LAUNCH();
 }

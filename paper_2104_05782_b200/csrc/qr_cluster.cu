@@ -402,6 +402,24 @@ void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, in
                double* scratch, int64_t scratch_elems) {
     const int64_t s = a.rows, w = a.cols, p = std::min(s, w);
     if (p == 0) return;
+    if (!qr_panel_fast(stream, a, tau)) hqr_panel_householder(stream, a, tau, scratch, scratch_elems);
+    if (twy) {
+        // Twy of the whole panel: Gram of W then the forward recurrence.
+        if (scratch_elems < s * p + p * p) throw Error(RUTV_ERR_INTERNAL, "hqr: scratch too small");
+        double* W = scratch;
+        double* Gm = W + s * p;
+        double* gw = Gm + p * p;
+        DView Wv(s, p, s, W), Gv(p, p, p, Gm);
+        make_w(stream, a, p, Wv);
+        gemm(stream, 1.0, Op::T, Wv, Op::N, Wv, 0.0, Gv, gw, scratch_elems - (gw - scratch));
+        form_t(stream, Gm, p, tau, p, twy, ldt);
+    }
+}
+
+void hqr_panel_householder(cudaStream_t stream, const DView& a, double* tau, double* scratch,
+                           int64_t scratch_elems) {
+    const int64_t s = a.rows, w = a.cols, p = std::min(s, w);
+    if (p == 0) return;
     const int cmax = max_cluster();
     const bool use_reg = reg_kernel_enabled() && qr_reg_capacity(s, cmax) >= std::min<int64_t>(w, 16);
     auto pick_reg = [&](int64_t rows, int64_t cols) {
@@ -449,17 +467,6 @@ void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, in
             gemm(stream, 1.0, Op::T, Tv, Op::N, Zv, 0.0, Z2v, gw, gw_elems);
             gemm(stream, -1.0, Op::N, Wv, Op::N, Z2v, 1.0, trail, gw, gw_elems);
         }
-    }
-    if (twy) {
-        // Twy of the whole panel: Gram of W then the forward recurrence.
-        if (scratch_elems < s * p + p * p) throw Error(RUTV_ERR_INTERNAL, "hqr: scratch too small");
-        double* W = scratch;
-        double* Gm = W + s * p;
-        double* gw = Gm + p * p;
-        DView Wv(s, p, s, W), Gv(p, p, p, Gm);
-        make_w(stream, a, p, Wv);
-        gemm(stream, 1.0, Op::T, Wv, Op::N, Wv, 0.0, Gv, gw, scratch_elems - (gw - scratch));
-        form_t(stream, Gm, p, tau, p, twy, ldt);
     }
 }
 

@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(kT, 1)
         if ((lane & 1) == 0) S.part[warp * KB + (lane >> 1)] = v;
         asm volatile("bar.sync 1, %0;" ::"r"(nwact * 32) : "memory");
         if (trace && tid == 0 && rank == 0 && jn < 64) trace[jn * 8 + 4] = clock64();
-        if (warp == 0) {
+        // every row-owning warp forms the (identical) message and sends it to
+        // its share of the destinations: warp w -> ranks w, w + nwact, ...
+        if (warp < CS) {
             double val = 0.0;
             if (lane < KB) {
                 for (int ww = 0; ww < nwact; ++ww) val += S.part[ww * KB + lane];
@@ -189,7 +191,8 @@ __global__ void __launch_bounds__(kT, 1)
             }
             const int par = jn & 1;
             const uint32_t off = msg_a + static_cast<uint32_t>(((par * CS + rank) * kMsg + lane) * 8);
-            for (int dst = 0; dst < CS; ++dst) st_async_f64(mapa_u32(off, dst), val, mapa_u32(bar0 + 8 * par, dst));
+            for (int dst = warp; dst < CS; dst += nwact)
+                st_async_f64(mapa_u32(off, dst), val, mapa_u32(bar0 + 8 * par, dst));
             if (trace && tid == 0 && rank == 0 && jn < 64) trace[jn * 8 + 5] = clock64();
         }
     };

@@ -126,9 +126,18 @@ void copy_upper(cudaStream_t stream, const DView& dst, const DView& src);
 void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, int64_t ldt,
                double* scratch, int64_t scratch_elems);
 int64_t hqr_work_elems(int64_t s, int64_t w);
+// The Householder kernels only (no Cholesky-QR2 fast path).
+void hqr_panel_householder(cudaStream_t stream, const DView& a, double* tau, double* scratch,
+                           int64_t scratch_elems);
 // Twy from the Gram matrix of W and tau (householder.cpp:76-97).
 void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* tau, int64_t p,
             double* t, int64_t ldt);
+
+// X = R^{-1} for upper triangular R (p <= 256), recursive doubling.
+void tri_inv_upper(cudaStream_t stream, const double* r, int64_t ldr, int64_t p, double* x, int64_t ldx);
+// Panel QR through Cholesky-QR2 + Householder reconstruction (cholqr.cu); false
+// (panel untouched) when the fast path is not applicable or not safe.
+bool qr_panel_fast(cudaStream_t stream, const DView& a, double* tau);
 
 // One-sided Jacobi SVD of a square block (jacobi_svd.cpp:39-148).  Writes U, sigma, V
 // (n x n, ld n).  Status (code, residual, kept, sweeps) is written to

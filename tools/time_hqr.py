@@ -20,7 +20,7 @@ shapes = [tuple(int(x) for x in s.split(",")) for s in sys.argv[1:]] or [
 for s, w in shapes:
     a0 = torch.randn(w, s, dtype=torch.float64, device="cuda").T
     tau = torch.zeros(w, dtype=torch.float64, device="cuda")
-    xs = [a0.T.contiguous().T for _ in range(6)]
+    xs = [a0.clone() for _ in range(6)]  # distinct panels (each call factors in place)
     hqr(xs[0], tau)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,6 +32,8 @@ for s, w in shapes:
     us = e0.elapsed_time(e1) * 1e3 / 5
     # device-side kernel time (CUPTI through torch.profiler)
     from torch.profiler import profile, ProfilerActivity
+    xs = [a0.clone() for _ in range(6)]  # fresh panels again for the profiled pass
+    torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for x in xs[1:]:
             hqr(x, tau)
