@@ -1,7 +1,7 @@
 """CPU test double of dist.CudaOps -- TEST INFRASTRUCTURE ONLY.
 
 Implements the same operations with torch CPU fp64 tensors and the CPU oracle
-(reference-convention Householder QR and Jacobi SVD), so the world_size-2
+(reference-convention Householder QR and Jacobi SVD), so the multi-rank
 gloo tests exercise the distributed schedule of paper_2104_05782_b200/dist.py
 end to end on CPU.  The product never uses this (CudaOps has no fallback).
 """
@@ -84,19 +84,19 @@ class TorchCpuOps:
             out.append((U, torch.from_numpy(s.copy()), V))
         return out
 
-    def all_reduce(self, x):
+    def all_reduce(self, x, comm):
         y = x.T.contiguous()
-        dist.all_reduce(y)
+        dist.all_reduce(y, group=comm.group)
         x.copy_(y.T)
 
-    def all_gather(self, x):
-        outs = [torch.zeros(x.shape[1], x.shape[0], dtype=torch.float64) for _ in range(dist.get_world_size())]
-        dist.all_gather(outs, x.T.contiguous())
+    def all_gather(self, x, comm):
+        outs = [torch.zeros(x.shape[1], x.shape[0], dtype=torch.float64) for _ in range(comm.size)]
+        dist.all_gather(outs, x.T.contiguous(), group=comm.group)
         return [o.T for o in outs]
 
-    def broadcast(self, x, src):
+    def broadcast(self, x, src, comm):
         y = x.T.contiguous() if x.dim() == 2 else x.contiguous()
-        dist.broadcast(y, src)
+        dist.broadcast(y, src, group=comm.group)
         x.copy_(y.T if x.dim() == 2 else y)
 
     def finish(self):

@@ -7,7 +7,7 @@ import paper_2104_05782_b200 as rutv
 def cm(m, n):
     return torch.empty((n, m), dtype=torch.float64, device="cuda").T
 
-def run(n, b, q, reps=3, profile=False):
+def run(n, b, q, reps=int(os.environ.get('REPS', '3')), profile=os.environ.get('PROFILE', '1') == '1'):
     a = cm(n, n); rutv.normal_fill(1, 0, a)
     t, u, v = cm(n, n), cm(n, n), cm(n, n)
     rutv.factorize_device(a, t, u, v, b=b, q=q, seed=2)  # warm
@@ -30,4 +30,4 @@ def run(n, b, q, reps=3, profile=False):
 
 for spec in sys.argv[1:]:
     n, b, q = (int(x) for x in spec.split(","))
-    run(n, b, q, profile=True)
+    run(n, b, q)
