@@ -14,7 +14,8 @@
  * RUTV_ERR_CONVERGENCE, and a message.  The codes map one-to-one onto the
  * reference's exception classes (proj/include/randutv/errors.hpp:9-50):
  * ConfigError -> RUTV_ERR_CONFIG, ShapeError -> RUTV_ERR_SHAPE,
- * IndexError -> RUTV_ERR_INDEX, ConvergenceError{residual} -> RUTV_ERR_CONVERGENCE.
+ * IndexError -> RUTV_ERR_INDEX, ConvergenceError{residual} -> RUTV_ERR_CONVERGENCE,
+ * IoError -> RUTV_ERR_IO.
  * The C++ shim (include/randutv_b200/randutv.hpp) rethrows those types.
  */
 #ifndef RUTV_B200_H
@@ -36,7 +37,8 @@ typedef enum {
     RUTV_ERR_NCCL = 6,
     RUTV_ERR_OOM = 7,
     RUTV_ERR_NOTIMPL = 8,
-    RUTV_ERR_INTERNAL = 9
+    RUTV_ERR_INTERNAL = 9,
+    RUTV_ERR_IO = 10          /* IoError                 (errors.hpp:36, matrix_io.cpp) */
 } rutv_code;
 
 typedef struct {
@@ -182,6 +184,25 @@ int rutv_b200_block_rows_async(double* small, int64_t lds_small, double* big, in
 /* Batched svd_block over count square problems; status = device double[4*count]. */
 int rutv_b200_svd_batch_async(int count, const int64_t* n, double* const* A, const int64_t* lda, double* const* U,
                               double* const* sigma, double* const* V, double* status, rutv_status* st);
+
+/* ---------------- data format and quality metrics (io_metrics.cu) ----------------
+ * .rutv files (proj/src/matrix_io.cpp:40-70): "RUTV", u64 LE rows, u64 LE cols,
+ * column-major binary64 payload, no trailing bytes.  Replace
+ * randutv::read_rutv / write_rutv (proj/include/randutv/matrix_io.hpp:12-13);
+ * failures are RUTV_ERR_IO with the reference's IoError messages.
+ * on_device != 0: `dst` / `src` are DEVICE pointers, streamed through pinned
+ * double buffers (disk I/O overlaps the host<->device copies). */
+int rutv_b200_rutv_dims(const char* path, int64_t* rows, int64_t* cols, rutv_status* st);
+int rutv_b200_read_rutv(const char* path, double* dst, int64_t ld, int on_device, rutv_status* st);
+int rutv_b200_write_rutv(const char* path, const double* src, int64_t rows, int64_t cols, int64_t ld, int on_device,
+                         rutv_status* st);
+/* randutv::lowrank_error (proj/src/metrics.cpp:32-46): ||A - U(:,0:k) T(0:k,:) V'|| of
+ * DEVICE matrices, norm 0 = Frobenius (matrix_ops.cpp:9-14), 1 = spectral estimate
+ * (matrix_ops.cpp:16-40; max_iter <= 0 selects the reference defaults 100, 1e-10).
+ * k outside [0, min(m, n)] -> RUTV_ERR_INDEX.  *out is a HOST double. */
+int rutv_b200_lowrank_error(int device, const double* A, int64_t lda, const double* T, int64_t ldt, const double* U,
+                            int64_t ldu, const double* V, int64_t ldv, int64_t m, int64_t n, int64_t k, int norm,
+                            int max_iter, double tol, double* out, rutv_status* st);
 
 #ifdef __cplusplus
 }

@@ -270,3 +270,110 @@ def form_wy_t(qr, tau) -> np.ndarray:
     twy = np.zeros((p, p), order="F")
     _lib("port").ora_form_wy_t(_p(qr), qr.shape[0], max(qr.shape[0], 1), _p(tau), p, _p(twy))
     return twy
+
+
+# ------------------------------------------------------------------ data format + metrics
+def rutv_bytes(a) -> bytes:
+    """matrix_io.cpp:40-50 restated: b"RUTV", u64 LE rows, u64 LE cols, column-major f64 LE."""
+    a = _f(a)
+    m, n = a.shape
+    return b"RUTV" + np.array([m, n], dtype="<u8").tobytes() + a.astype("<f8").tobytes(order="F")
+
+
+def parse_rutv(data: bytes) -> np.ndarray:
+    """matrix_io.cpp:52-70 restated (same checks, IoError -> OSError with the reference's text)."""
+    if len(data) < 4 or data[:4] != b"RUTV":
+        raise OSError("bad magic")
+    if len(data) < 20:
+        raise OSError("truncated header")
+    m, n = (int(x) for x in np.frombuffer(data[4:20], dtype="<u8"))
+    if m > (1 << 30) or n > (1 << 30):
+        raise OSError("implausible dimensions")
+    need = 20 + 8 * m * n
+    if len(data) < need:
+        raise OSError("truncated header")
+    if len(data) > need:
+        raise OSError("trailing bytes")
+    return np.frombuffer(data[20:need], dtype="<f8").reshape((n, m)).T.copy(order="F")
+
+
+def lowrank_error(a, t, u, v, k: int, norm: str = "fro") -> float:
+    """metrics.cpp:32-46 restated in numpy: ||A - U(:,0:k) T(0:k,:) V'||, Frobenius
+    (matrix_ops.cpp:9-14) or the spectral power-iteration estimate (matrix_ops.cpp:16-40)."""
+    a, t, u, v = _f(a), _f(t), _f(u), _f(v)
+    m, n = a.shape
+    if k < 0 or k > min(m, n):
+        raise IndexError("lowrank_error: rank out of range")
+    e = a - u[:, :k] @ (t[:k, :] @ v.T)
+    if norm == "fro":
+        return float(np.sqrt(np.sum(e * e)))
+    if e.size == 0:
+        return 0.0
+    x = normal_stream(0x5EEDB0B5, 0, n).reshape(n, 1)
+    nx = float(np.sqrt(np.sum(x * x)))
+    if nx == 0.0:
+        return 0.0
+    x /= nx
+    est = 0.0
+    for it in range(100):
+        y = e @ x
+        x = e.T @ y
+        ny = float(np.sqrt(np.sum(x * x)))
+        if ny == 0.0:
+            return 0.0
+        nxt = float(np.sqrt(ny))
+        x /= ny
+        if it > 0 and abs(nxt - est) <= 1e-10 * nxt:
+            return nxt
+        est = nxt
+    return est
+
+
+def optimal_error(sigma, k: int, norm: str = "fro") -> float:
+    """metrics.cpp:48-58: sigma_{k+1} (spectral) or sqrt(sum_{i>k} sigma_i^2), summed from the tail."""
+    sigma = np.asarray(sigma, dtype=np.float64)
+    if k < 0:
+        raise IndexError("optimal_error: negative rank")
+    if k >= sigma.size:
+        return 0.0
+    if norm != "fro":
+        return float(sigma[k])
+    s = 0.0
+    for i in range(sigma.size - 1, k - 1, -1):
+        s += sigma[i] * sigma[i]
+    return float(np.sqrt(s))
+
+
+def ref_write_rutv(path: str, a) -> None:
+    a = _f(a)
+    L = _lib("ref")
+    L.ref_write_rutv.argtypes = [C.c_char_p, _D, _I64, _I64, _I64]
+    rc = L.ref_write_rutv(path.encode(), _p(a), a.shape[0], a.shape[1], max(a.shape[0], 1))
+    if rc != 0:
+        raise OracleError(rc)
+
+
+def ref_read_rutv(path: str) -> np.ndarray:
+    L = _lib("ref")
+    L.ref_read_rutv.argtypes = [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64), _D]
+    m, n = _I64(0), _I64(0)
+    rc = L.ref_read_rutv(path.encode(), C.byref(m), C.byref(n), None)
+    if rc != 0:
+        raise OracleError(rc)
+    out = np.zeros((m.value, n.value), order="F")
+    rc = L.ref_read_rutv(path.encode(), C.byref(m), C.byref(n), _p(out))
+    if rc != 0:
+        raise OracleError(rc)
+    return out
+
+
+def ref_lowrank_error(a, t, u, v, k: int, norm: str = "fro") -> float:
+    a, t, u, v = _f(a), _f(t), _f(u), _f(v)
+    L = _lib("ref")
+    L.ref_lowrank_error.argtypes = [_D, _D, _D, _D, _I64, _I64, _I64, C.c_int, _D]
+    out = C.c_double(0.0)
+    rc = L.ref_lowrank_error(_p(a), _p(t), _p(u), _p(v), a.shape[0], a.shape[1], k, int(norm != "fro"),
+                             C.byref(out))
+    if rc != 0:
+        raise OracleError(rc)
+    return out.value

@@ -22,6 +22,7 @@
 #include "randutv/householder.hpp"
 #include "randutv/jacobi_svd.hpp"
 #include "randutv/matrix.hpp"
+#include "randutv/matrix_io.hpp"
 #include "randutv/matrix_ops.hpp"
 #include "randutv/metrics.hpp"
 #include "randutv/randutv_blocked.hpp"
@@ -43,6 +44,8 @@ int status_of(const std::exception_ptr& p, double* residual) {
     } catch (const ConvergenceError& e) {
         if (residual) *residual = e.residual;
         return 4;
+    } catch (const IoError&) {
+        return 10;
     } catch (const std::bad_alloc&) {
         return 7;
     } catch (...) {
@@ -216,6 +219,43 @@ int ref_gemm(double alpha, int ta, const double* a, int64_t ar, int64_t ac, int6
         gemm(alpha, ta ? Trans::T : Trans::N, ConstMatrixView(ar, ac, lda, a),
              tb ? Trans::T : Trans::N, ConstMatrixView(br, bc, ldb, b), beta,
              MatrixView(m, n, ldc, c));
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception(), nullptr);
+    }
+}
+
+// .rutv I/O (matrix_io.cpp:40-70).  ref_read_rutv: dims when out == nullptr.
+int ref_write_rutv(const char* path, const double* a, int64_t m, int64_t n, int64_t lda) {
+    try {
+        write_rutv(path, ConstMatrixView(m, n, lda, a));
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception(), nullptr);
+    }
+}
+
+int ref_read_rutv(const char* path, int64_t* m, int64_t* n, double* out) {
+    try {
+        Matrix r = read_rutv(path);
+        *m = r.rows();
+        *n = r.cols();
+        if (out) put(out, r);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception(), nullptr);
+    }
+}
+
+// lowrank_error (metrics.cpp:32-46) with square U (m x m), T (m x n), V (n x n).
+int ref_lowrank_error(const double* a, const double* t, const double* u, const double* v, int64_t m, int64_t n,
+                      int64_t k, int spectral, double* out) {
+    try {
+        UTVResult r;
+        r.t = to_matrix(ConstMatrixView(m, n, m, t));
+        r.u = to_matrix(ConstMatrixView(m, m, m, u));
+        r.v = to_matrix(ConstMatrixView(n, n, n, v));
+        *out = lowrank_error(ConstMatrixView(m, n, m, a), r, k, spectral ? Norm::Spectral : Norm::Frobenius);
         return 0;
     } catch (...) {
         return status_of(std::current_exception(), nullptr);

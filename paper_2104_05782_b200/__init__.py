@@ -25,10 +25,12 @@ LIB_PATH = os.path.join(HERE, "librutv_b200.so")
 
 __all__ = ["factorize", "factorize_device", "flops", "stream_length", "ConvergenceError",
            "RutvError", "lib", "gemm", "hqr", "svd_block", "normal_fill", "apply_q_right",
-           "apply_qt_left", "launch_count", "last_profile"]
+           "apply_qt_left", "launch_count", "last_profile", "read_rutv", "write_rutv", "lowrank_error",
+           "optimal_error", "quality_report", "to_csv"]
 
 RUTV_OK, RUTV_ERR_CONFIG, RUTV_ERR_SHAPE, RUTV_ERR_INDEX, RUTV_ERR_CONVERGENCE = 0, 1, 2, 3, 4
 RUTV_ERR_CUDA, RUTV_ERR_NCCL, RUTV_ERR_OOM, RUTV_ERR_NOTIMPL, RUTV_ERR_INTERNAL = 5, 6, 7, 8, 9
+RUTV_ERR_IO = 10
 
 
 class RutvError(RuntimeError):
@@ -114,6 +116,12 @@ def lib() -> C.CDLL:
     L.rutv_b200_block_rows_async.argtypes = [V, _I64, V, _I64, _I64, _I64, _I64, _I64, _I64, _I64, C.c_int, S]
     L.rutv_b200_svd_batch_async.argtypes = [C.c_int, C.POINTER(_I64), C.POINTER(V), C.POINTER(_I64),
                                             C.POINTER(V), C.POINTER(V), C.POINTER(V), V, S]
+    # data format + quality metrics (io_metrics.cu)
+    L.rutv_b200_rutv_dims.argtypes = [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64), S]
+    L.rutv_b200_read_rutv.argtypes = [C.c_char_p, V, _I64, C.c_int, S]
+    L.rutv_b200_write_rutv.argtypes = [C.c_char_p, V, _I64, _I64, _I64, C.c_int, S]
+    L.rutv_b200_lowrank_error.argtypes = [C.c_int, V, _I64, V, _I64, V, _I64, V, _I64, _I64, _I64, _I64, C.c_int,
+                                          C.c_int, C.c_double, _D, S]
     _lib = L
     return L
 
@@ -126,6 +134,8 @@ def _raise(st: Status) -> None:
         raise ValueError(msg)
     if st.code == RUTV_ERR_INDEX:
         raise IndexError(msg)
+    if st.code == RUTV_ERR_IO:  # IoError -> OSError (bindings.cpp:109-121)
+        raise OSError(msg)
     if st.code == RUTV_ERR_CONVERGENCE:
         raise ConvergenceError(st.code, msg, st.residual)
     raise RutvError(st.code, msg, st.residual)
@@ -317,3 +327,99 @@ def spectrum_matrix_device(a, seed: int, sigma=None, beta: float = 1.0) -> None:
     st = Status()
     lib().rutv_b200_spectrum_matrix(a.device.index, m, n, sp, beta, seed, pa, lda, C.byref(st))
     _raise(st)
+
+
+# ----------------------------------------------------------------- data format + metrics
+def _is_cuda(x) -> bool:
+    return hasattr(x, "is_cuda") and x.is_cuda
+
+
+def write_rutv(path: str, a) -> None:
+    """randutv::write_rutv (proj/src/matrix_io.cpp:40-50) from a host array or a CUDA
+    tensor (column-major or any 2-D layout; device tensors stream through pinned buffers)."""
+    st = Status()
+    if _is_cuda(a):
+        x = a if a.stride(0) == 1 else a.T.contiguous().T  # column-major view
+        ld = max(x.stride(1) if x.shape[1] > 1 else x.shape[0], x.shape[0], 1)
+        lib().rutv_b200_write_rutv(os.fsencode(path), C.c_void_p(x.data_ptr()), x.shape[0], x.shape[1], ld, 1,
+                                   C.byref(st))
+    else:
+        x = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        lib().rutv_b200_write_rutv(os.fsencode(path), _ptr(x), x.shape[0], x.shape[1], max(x.shape[0], 1), 0,
+                                   C.byref(st))
+    _raise(st)
+
+
+def read_rutv(path: str, device=None):
+    """randutv::read_rutv (proj/src/matrix_io.cpp:52-70).  ``device=None``: a Fortran-ordered
+    numpy array; else a column-major CUDA tensor on that device (payload streamed to HBM)."""
+    st = Status()
+    m, n = _I64(0), _I64(0)
+    lib().rutv_b200_rutv_dims(os.fsencode(path), C.byref(m), C.byref(n), C.byref(st))
+    _raise(st)
+    m, n = m.value, n.value
+    if device is None:
+        out = np.zeros((m, n), order="F")
+        lib().rutv_b200_read_rutv(os.fsencode(path), _ptr(out), max(m, 1), 0, C.byref(st))
+    else:
+        import torch
+        out = torch.empty((n, m), dtype=torch.float64, device=device).T
+        lib().rutv_b200_read_rutv(os.fsencode(path), C.c_void_p(out.data_ptr()), max(m, 1), 1, C.byref(st))
+    _raise(st)
+    return out
+
+
+def lowrank_error(a, t, u, v, k: int, norm: str = "fro") -> float:
+    """randutv::lowrank_error (proj/src/metrics.cpp:32-46) on the device: CUDA tensors
+    A (m x n), T (m x n), U (m x m), V (n x n); norm "fro" or "spectral"."""
+    st = Status()
+    out = C.c_double(0.0)
+    pa, pt, pu, pv = (_cm(x) for x in (a, t, u, v))
+    m, n = a.shape
+    if t.shape != (m, n) or u.shape != (m, m) or v.shape != (n, n):
+        raise ValueError("lowrank_error: needs square U and V matching A")
+    lib().rutv_b200_lowrank_error(a.device.index or 0, pa[0], pa[3], pt[0], pt[3], pu[0], pu[3], pv[0], pv[3], m, n,
+                                  int(k), 0 if norm == "fro" else 1, 0, 0.0, C.byref(out), C.byref(st))
+    _raise(st)
+    return out.value
+
+
+def optimal_error(sigma, k: int, norm: str = "fro") -> float:
+    """randutv::optimal_error (metrics.cpp:48-58) from known singular values."""
+    sig = np.asarray(sigma, dtype=np.float64)
+    if k < 0:
+        raise IndexError("optimal_error: negative rank")
+    if k >= sig.size:
+        return 0.0
+    if norm != "fro":
+        return float(sig[k])
+    tail = sig[k:][::-1]
+    return float(np.sqrt(np.sum(tail * tail)))
+
+
+def quality_report(a, t, u, v, ks, sigma, norm: str = "fro") -> list[dict]:
+    """randutv::quality_report (metrics.cpp:161-184) with the residuals on the device.
+    ``sigma``: the singular values of A (known by construction for the spectrum
+    generators; the reference computes them with a dense Jacobi SVD)."""
+    p = min(a.shape)
+    sig = np.asarray(sigma, dtype=np.float64)
+    diag = t.diagonal().double().cpu().numpy() if _is_cuda(t) else np.diag(t)
+    rows = []
+    for k in ks:
+        if k < 1 or k > p:
+            raise IndexError("quality_report: ranks must satisfy 1 <= k <= min(m, n)")
+        e_utv = lowrank_error(a, t, u, v, k, norm)
+        e_opt = optimal_error(sig, k, norm)
+        ratio = e_utv / e_opt if e_opt > 0 else (1.0 if e_utv == 0 else float("inf"))
+        s, d = sig[k - 1], diag[k - 1]
+        rows.append({"k": int(k), "err_utv": e_utv, "err_opt": e_opt, "ratio": ratio,
+                     "diag_relerr": abs(d - s) / s if s > 0 else abs(d)})
+    return rows
+
+
+def to_csv(rows: list[dict]) -> str:
+    """metrics.cpp:186-197: header k,err_utv,err_opt,ratio,diag_relerr, %.17g values."""
+    out = ["k,err_utv,err_opt,ratio,diag_relerr"]
+    for r in rows:
+        out.append("%d,%s,%s,%s,%s" % (r["k"], *("%.17g" % r[c] for c in ("err_utv", "err_opt", "ratio", "diag_relerr"))))
+    return "\n".join(out) + "\n"

@@ -95,6 +95,16 @@ def main() -> None:
         t, u, v = oracle.randutv(a, b=b, q=q, seed=sg, impl="ref")
         np.savez_compressed(os.path.join(OUT, f"randutv_{name}.npz"), a=a, t=t, u=u, v=v,
                             meta=np.array([m, n, b, q, sg], dtype=np.int64))
+    # .rutv files written by the reference (matrix_io.cpp:40-50) + lowrank_error values
+    # (metrics.cpp:32-46) for the r64 factorization, Frobenius and spectral
+    oracle.ref_write_rutv(os.path.join(OUT, "g5x3.rutv"), oracle.gaussian_matrix(5, 3, 77, impl="ref"))
+    oracle.ref_write_rutv(os.path.join(OUT, "empty0x4.rutv"), np.zeros((0, 4)))
+    r = np.load(os.path.join(OUT, "randutv_r64_b16_q2.npz"))
+    ks = np.array([0, 1, 8, 16, 33, 63, 64])
+    np.savez_compressed(os.path.join(OUT, "lowrank_r64.npz"), ks=ks,
+                        fro=np.array([oracle.ref_lowrank_error(r["a"], r["t"], r["u"], r["v"], k) for k in ks]),
+                        spec=np.array([oracle.ref_lowrank_error(r["a"], r["t"], r["u"], r["v"], k, "spec")
+                                       for k in ks]))
     print("golden fixtures written to", OUT)
 
 
