@@ -12,11 +12,17 @@
 //   * smem tiles stored in the operand's contiguous global direction with a
 //     +4-double pad so every fragment load is bank-conflict free for all four
 //     transpose combinations;
-//   * two CTA tiles: 128x128 (8 warps, 64x32 warp tiles) for the large
-//     rank-b updates, 64x64 (4 warps) + deterministic split-K for the
-//     tall-skinny K = s sketch / projection products;
+//   * main tile 128 x 64, 4 warps of 64 x 32, BK = 16, two CTAs per SM: one
+//     CTA's k-tile barrier and epilogue hide behind the other's DMMAs; with
+//     beta != 0 the C tile is staged through shared memory by cp.async (all
+//     loads in flight at once) instead of per-element register loads;
+//   * 64 x 64 tiles (4 warps of 32 x 32, C prefetched into registers) with a
+//     deterministic split-K for the skinny K = s products (one side = b);
 //   * split-K partials are summed in a fixed order by a separate kernel, so
 //     results are bit-reproducible run to run.
+// Measured (tools/gemm_bench.py, profiles/r01_gemm_sweep.jsonl): 32.5 TF/s at
+// 8192^3 (88% of the DMMA peak; cuBLAS's sm_80 d884 kernel 35.5), 21.7 at the
+// rank-128 update 4000^2 x 128, 30.5 at 20000^2 x 512.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -109,6 +115,7 @@ struct GemmParams {
     double* work;
     int64_t kchunk;
     int splits;
+    int cvec;  // C 16-byte aligned with an even ldc: 16-byte cp.async for the C tile
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -141,10 +148,21 @@ struct SmemGeom {
     static constexpr int A_SZ = TA ? BM * A_LD : BK * A_LD;
     static constexpr int B_LD = TB ? (BN + 4) : (BK + 4);
     static constexpr int B_SZ = TB ? BK * B_LD : BN * B_LD;
+    static constexpr int C_LD = BM + 4;  // (2 C_LD) mod 16 == 8: conflict-free fragment reads
+    static constexpr int C_SZ = BN * C_LD;
 };
 
+// Large warp tiles read C in the epilogue through shared memory (see below).
+template <int WM, int WN>
+constexpr bool gemm_prefetch_c() { return (WM / 16) * (WN / 8) * 4 <= 32; }
+
+// Resident CTAs per SM the tile is built for: 4-warp tiles run two CTAs per SM
+// so one CTA's k-tile barrier and epilogue hide behind the other's DMMAs.
+template <int BM, int BN, int WM, int WN>
+constexpr int gemm_min_blocks() { return (BM / WM) * (BN / WN) <= 4 ? 2 : 1; }
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, bool VEC>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, (gemm_min_blocks<BM, BN, WM, WN>()))
     dgemm_kernel(const GemmParams p) {
     constexpr int NWM = BM / WM, NWN = BN / WN, NT = NWM * NWN * 32;
     constexpr int MI = WM / 16, NI = WN / 8;
@@ -265,19 +283,24 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
     // beta != 0: prefetch this thread's C fragment now so the epilogue's
     // read-modify-write does not serialise on global-load latency (the
     // rank-b updates have K = b, a mainloop of only a few k-tiles).
+    // (Large warp tiles would need 2x the accumulator registers for it: they
+    // read C in the epilogue and rely on the second resident CTA instead.)
+    constexpr bool PRE = gemm_prefetch_c<WM, WN>();
     const bool direct = p.splits == 1;
     const bool use_c = direct && p.beta != 0.0;
-    double cpre[MI][NI][4];
+    double cpre[PRE ? MI : 1][PRE ? NI : 1][4];
+    if constexpr (PRE) {
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni)
+            for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int64_t m = m0 + wm * WM + mi * 16 + g + (r >= 2 ? 8 : 0);
-                const int64_t n = n0 + wn * WN + ni * 8 + 2 * t + (r & 1);
-                cpre[mi][ni][r] = (use_c && m < M && n < N) ? __ldg(p.C + m + n * p.ldc) : 0.0;
-            }
+                for (int r = 0; r < 4; ++r) {
+                    const int64_t m = m0 + wm * WM + mi * 16 + g + (r >= 2 ? 8 : 0);
+                    const int64_t n = n0 + wn * WN + ni * 8 + 2 * t + (r & 1);
+                    cpre[mi][ni][r] = (use_c && m < M && n < N) ? __ldg(p.C + m + n * p.ldc) : 0.0;
+                }
+    }
 
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
@@ -316,6 +339,68 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
     cp_async_wait<0>();
 
     double* wbase = p.work + static_cast<int64_t>(blockIdx.z) * M * N;
+    // beta != 0 without the register prefetch: the C tile is staged through
+    // shared memory (the pipeline stages are free now) with every cp.async in
+    // flight at once -- register pressure would otherwise make the compiler
+    // serialise one HBM round trip per element.  The second resident CTA of
+    // the SM keeps the DMMA pipe busy meanwhile.
+    if constexpr (!PRE) {
+        if (use_c) {
+            __syncthreads();  // every warp is done with the last k-tile
+            double* cs = smem;
+            if (p.cvec) {
+                for (int c = tid; c < BN * (BM / 2); c += NT) {
+                    const int nn = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+                    const int64_t gm = m0 + mm, gn = n0 + nn;
+                    int bytes = 0;
+                    const double* src = p.C;
+                    if (gn < N && gm < M) {
+                        bytes = gm + 1 < M ? 16 : 8;
+                        src = p.C + gm + gn * p.ldc;
+                    }
+                    cp_async16(cs + nn * G::C_LD + mm, src, bytes);
+                }
+            } else {
+                for (int c = tid; c < BN * BM; c += NT) {
+                    const int nn = c / BM, mm = c % BM;
+                    const int64_t gm = m0 + mm, gn = n0 + nn;
+                    const bool ok = gn < N && gm < M;
+                    cp_async8(cs + nn * G::C_LD + mm, ok ? p.C + gm + gn * p.ldc : p.C, ok ? 8 : 0);
+                }
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int ml = wm * WM + mi * 16 + g + (r >= 2 ? 8 : 0);
+                        const int nl = wn * WN + ni * 8 + 2 * t + (r & 1);
+                        acc[mi][ni][r] = p.alpha * acc[mi][ni][r] + p.beta * cs[nl * G::C_LD + ml];
+                    }
+        } else if (direct) {
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc[mi][ni][r] *= p.alpha;
+        }
+    } else if (direct) {
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    double v = p.alpha * acc[mi][ni][r];
+                    if (use_c) v += p.beta * cpre[mi][ni][r];
+                    acc[mi][ni][r] = v;
+                }
+    }
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -325,13 +410,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
                 const int64_t m = m0 + wm * WM + mi * 16 + g + (r >= 2 ? 8 : 0);
                 const int64_t n = n0 + wn * WN + ni * 8 + 2 * t + (r & 1);
                 if (m < M && n < N) {
-                    if (direct) {
-                        double v = p.alpha * acc[mi][ni][r];
-                        if (use_c) v += p.beta * cpre[mi][ni][r];
-                        p.C[m + n * p.ldc] = v;
-                    } else {
+                    if (direct)
+                        p.C[m + n * p.ldc] = acc[mi][ni][r];
+                    else
                         wbase[m + n * M] = acc[mi][ni][r];
-                    }
                 }
             }
 }
@@ -366,7 +448,9 @@ namespace {
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool TA, bool TB, bool VEC>
 void launch_cfg(cudaStream_t stream, const GemmParams& p, int gx, int gy, int gz) {
     using G = SmemGeom<BM, BN, BK, TA, TB>;
-    constexpr int smem = ST * (G::A_SZ + G::B_SZ) * static_cast<int>(sizeof(double));
+    constexpr int stages = ST * (G::A_SZ + G::B_SZ);
+    constexpr int smem = (gemm_prefetch_c<WM, WN>() || stages >= G::C_SZ ? stages : G::C_SZ) *
+                         static_cast<int>(sizeof(double));
     constexpr int nt = (BM / WM) * (BN / WN) * 32;
     auto kern = dgemm_kernel<BM, BN, BK, WM, WN, ST, TA, TB, VEC>;
     static bool configured = false;  // per instantiation
@@ -408,25 +492,46 @@ constexpr int kBK = 16;
 // the output tiles -- times a split-K factor for long K -- fill about one
 // wave of 148 SMs; otherwise 64x64 tiles (several CTAs/SM) with split-K.
 struct GemmPlan {
-    bool large;
+    bool large;  // 128 x 64 tiles (4 warps, 2 CTAs/SM); else 64 x 64 (legacy plan only)
     int splits;
 };
 
+int gemm_plan_mode() {  // RUTV_GEMM_PLAN=1: the 64 x 64 split-K plan for every short-tile product
+    static int m = [] {
+        const char* e = std::getenv("RUTV_GEMM_PLAN");
+        return e ? std::atoi(e) : 0;
+    }();
+    return m;
+}
+
+// Tile + deterministic split-K plan.  128 x 64 tiles run two CTAs per SM
+// (296 slots).  Enough tiles (>= 3 waves) or a short K (the rank-b updates):
+// no split.  Otherwise (the K = s sketch / projection products, m or n = b)
+// split K so the launch fills about two waves, each split at least 256 deep.
 GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t work_elems) {
-    const int64_t tl = ((M + 127) / 128) * ((N + 127) / 128);
-    if (tl >= kNumSMs) return {true, 1};
     auto cap = [&](int64_t sp) {
         if (M * N > 0) sp = std::min<int64_t>(sp, work_elems / (M * N));
         return static_cast<int>(std::max<int64_t>(sp, 1));
     };
-    // (128x128 tiles + split-K measured slower than 64x64 + split-K on the
-    // tall-skinny K = s products: one 8-warp CTA per SM hides less latency.)
-    const int64_t ts = ((M + 63) / 64) * ((N + 63) / 64);
-    const int64_t want = 3 * kNumSMs;
-    if (ts >= want || K < 512) return {false, 1};
-    int64_t sp = (want + ts - 1) / ts;
-    sp = std::min<int64_t>({sp, K / 128, 32});
-    return {false, cap(sp)};
+    // Skinny products (one side <= 128, i.e. n x b with b <= 128) keep the
+    // 64 x 64 split-K plan: measured 22 vs 18.8 TF/s at 4000 x 128 x 4000.
+    if (gemm_plan_mode() == 1 || (std::min(M, N) <= 128 && K >= 512)) {
+        const int64_t tl = ((M + 127) / 128) * ((N + 127) / 128);
+        if (tl >= kNumSMs) return {true, 1};
+        const int64_t ts = ((M + 63) / 64) * ((N + 63) / 64);
+        const int64_t want = 3 * kNumSMs;
+        if (ts >= want || K < 512) return {false, 1};
+        int64_t sp = (want + ts - 1) / ts;
+        sp = std::min<int64_t>({sp, K / 128, 32});
+        return {false, cap(sp)};
+    }
+    const int64_t slots = 2 * kNumSMs;
+    const int64_t tb = ((M + 127) / 128) * ((N + 63) / 64);
+    if (K < 1024 && tb < slots) return {false, 1};  // small late-step updates: more, smaller tiles
+    if (tb >= 3 * slots || K < 1024) return {true, 1};
+    int64_t sp = (2 * slots + tb - 1) / tb;
+    sp = std::min<int64_t>({sp, K / 256, 32});
+    return {true, cap(sp)};
 }
 
 }  // namespace
@@ -457,7 +562,8 @@ void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const
         return;
     }
     ProfScope prof(stream, 2.0 * static_cast<double>(M) * N * K);
-    GemmParams p{M, N, K, a.data, a.ld, b.data, b.ld, c.data, c.ld, alpha, beta, work, K, 1};
+    GemmParams p{M, N, K, a.data, a.ld, b.data, b.ld, c.data, c.ld, alpha, beta, work, K, 1,
+                 aligned16(c.data, c.ld) ? 1 : 0};
     const bool vec = aligned16(a.data, a.ld) && aligned16(b.data, b.ld);
     const bool tA = ta == Op::T, tB = tb == Op::T;
     const GemmPlan pl = plan_gemm(M, N, K, work ? work_elems : 0);
@@ -469,35 +575,23 @@ void gemm(cudaStream_t stream, double alpha, Op ta, const DView& a, Op tb, const
         p.kchunk = kc;
         p.splits = splits;
     }
-    if (pl.large)
-    {
+    if (pl.large) {
         static int cfg = [] {
             const char* e = std::getenv("RUTV_GEMM_CFG");
-            return e ? std::atoi(e) : 2;
+            return e ? std::atoi(e) : 4;
         }();
-        // cfg 2 (16 warps of 32x32, BK = 32, 3 stages) measured best on B200:
-        // 27.9 TF/s at 8192^3 vs 24.4 for 8 warps of 64x32 (tools/gemmsweep.sh).
-        if (cfg == 1)
-            dispatch<128, 128, 16, 32, 32, 4>(stream, p, tA, tB, vec, splits);
-        else if (cfg == 0)
-            dispatch<128, 128, kBK, 64, 32, 3>(stream, p, tA, tB, vec, splits);
-        else
+        // cfg 4 (128 x 64, 4 warps of 64 x 32, BK = 16, 3 stages, 2 CTAs/SM,
+        // C staged through shared memory) measured best on B200 for every step
+        // shape (tools/gemm_bench.py: 32.5 TF/s at 8192^3, 21.7 at K = 128,
+        // 30.5 at 20000^2 x 512) over cfg 2 (128 x 128, 16 warps) and cfg 3.
+        if (cfg == 2)
             dispatch<128, 128, 32, 32, 32, 3>(stream, p, tA, tB, vec, splits);
-    }
-    else
-    {
-        static int scfg = [] {
-            const char* e = std::getenv("RUTV_GEMM_SCFG");
-            return e ? std::atoi(e) : 0;
-        }();
-        if (scfg == 1)
-            dispatch<64, 64, 32, 32, 32, 3>(stream, p, tA, tB, vec, splits);
-        else if (scfg == 2)
-            dispatch<64, 64, 32, 32, 16, 3>(stream, p, tA, tB, vec, splits);
-        else if (scfg == 3)
-            dispatch<64, 64, 16, 32, 32, 4>(stream, p, tA, tB, vec, splits);
+        else if (cfg == 3)
+            dispatch<64, 128, 16, 32, 64, 3>(stream, p, tA, tB, vec, splits);
         else
-            dispatch<64, 64, kBK, 32, 32, 3>(stream, p, tA, tB, vec, splits);
+            dispatch<128, 64, 16, 64, 32, 3>(stream, p, tA, tB, vec, splits);
+    } else {
+        dispatch<64, 64, kBK, 32, 32, 3>(stream, p, tA, tB, vec, splits);
     }
     if (splits > 1) {
         const int64_t total = M * N;
