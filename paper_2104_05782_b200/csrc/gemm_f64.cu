@@ -508,30 +508,50 @@ int gemm_plan_mode() {  // RUTV_GEMM_PLAN=1: the 64 x 64 split-K plan for every 
 // (296 slots).  Enough tiles (>= 3 waves) or a short K (the rank-b updates):
 // no split.  Otherwise (the K = s sketch / projection products, m or n = b)
 // split K so the launch fills about two waves, each split at least 256 deep.
+// Split count for `tiles` output tiles over K: minimise a wave model --
+// ceil(tiles * sp / slots) waves of CTAs that each run K / sp deep (DMMA time
+// at half an SM, plus a fixed prologue / epilogue cost), plus the split-K
+// reduction's HBM traffic (sp partial M x N planes read, C written).
+int choose_splits(int64_t M, int64_t N, int64_t K, int64_t tiles, int64_t tile_flops_per_k, int64_t slots,
+                  int64_t maxsp) {
+    const double clk = 1.965e9, sm_rate = 127.6 / 2.0;  // flop/clk for one of two resident CTAs
+    double best = 1e300;
+    int bsp = 1;
+    for (int64_t sp = 1; sp <= maxsp; ++sp) {
+        const double chunk = static_cast<double>((K + sp - 1) / sp);
+        const double waves = static_cast<double>((tiles * sp + slots - 1) / slots);
+        const double t_cta = chunk * static_cast<double>(tile_flops_per_k) / sm_rate / clk + 2.0e-6;
+        const double t_red = sp > 1 ? static_cast<double>(sp + 2) * M * N * 8.0 / 6.0e12 + 3.0e-6 : 0.0;
+        const double t = waves * t_cta + t_red;
+        if (t < best * 0.98) {  // more splits only for a clear win
+            best = t;
+            bsp = static_cast<int>(sp);
+        }
+    }
+    return bsp;
+}
+
+// Tile + deterministic split-K plan.  128 x 64 tiles run two CTAs per SM
+// (296 slots).  Enough tiles (>= 3 waves) or a short K (the rank-b updates):
+// no split.  Otherwise (the K = s sketch / projection products, m or n = b)
+// split K by the wave model above.
 GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t work_elems) {
     auto cap = [&](int64_t sp) {
         if (M * N > 0) sp = std::min<int64_t>(sp, work_elems / (M * N));
         return static_cast<int>(std::max<int64_t>(sp, 1));
     };
-    // Skinny products (one side <= 128, i.e. n x b with b <= 128) keep the
-    // 64 x 64 split-K plan: measured 22 vs 18.8 TF/s at 4000 x 128 x 4000.
-    if (gemm_plan_mode() == 1 || (std::min(M, N) <= 128 && K >= 512)) {
-        const int64_t tl = ((M + 127) / 128) * ((N + 127) / 128);
-        if (tl >= kNumSMs) return {true, 1};
-        const int64_t ts = ((M + 63) / 64) * ((N + 63) / 64);
-        const int64_t want = 3 * kNumSMs;
-        if (ts >= want || K < 512) return {false, 1};
-        int64_t sp = (want + ts - 1) / ts;
-        sp = std::min<int64_t>({sp, K / 128, 32});
-        return {false, cap(sp)};
-    }
     const int64_t slots = 2 * kNumSMs;
+    // Skinny products (one side <= 128, i.e. n x b with b <= 128): 64 x 64
+    // tiles (measured 22 vs 18.8 TF/s for 128 x 64 at 4000 x 128 x 4000).
+    if (gemm_plan_mode() == 1 || (std::min(M, N) <= 128 && K >= 512)) {
+        const int64_t ts = ((M + 63) / 64) * ((N + 63) / 64);
+        if (K < 512) return {false, 1};
+        return {false, cap(choose_splits(M, N, K, ts, 64 * 64 * 2, slots, std::min<int64_t>(K / 128, 32)))};
+    }
     const int64_t tb = ((M + 127) / 128) * ((N + 63) / 64);
     if (K < 1024 && tb < slots) return {false, 1};  // small late-step updates: more, smaller tiles
     if (tb >= 3 * slots || K < 1024) return {true, 1};
-    int64_t sp = (2 * slots + tb - 1) / tb;
-    sp = std::min<int64_t>({sp, K / 256, 32});
-    return {true, cap(sp)};
+    return {true, cap(choose_splits(M, N, K, tb, 128 * 64 * 2, slots, std::min<int64_t>(K / 256, 32)))};
 }
 
 }  // namespace

@@ -363,6 +363,8 @@ __global__ void __launch_bounds__(kT, 1)
         __syncthreads();
         if (j0 + kt >= w) continue;
 
+        const int tph = phase;
+        if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 0] = clock64();
         // ---- block phase: A_t <- A_t - V T' (V' A_t), A_t = columns [j0 + kt, w)
         const int nrest = w - j0 - kt, ncol = KB + nrest;
         const int lo = min(rc, max(0, j0 - r_beg));  // local rows with gi >= j0
@@ -375,8 +377,8 @@ __global__ void __launch_bounds__(kT, 1)
                 const int tile = u % nt, ks = u / nt;
                 const int kb0 = (ks * nk4) / ksplit, kb1 = ((ks + 1) * nk4) / ksplit;
                 const int q = tile * 8 + g;  // my B column
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                for (int k4 = kb0; k4 < kb1; ++k4) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0}, acc2[4] = {0.0, 0.0, 0.0, 0.0};
+                auto slow = [&](int k4) {  // rows in the unit-triangle zone or past rc
                     const int li = lo + 4 * k4 + t4, gi = r_beg + li;
                     const double a0 = vent(S.chunk, LD, li, rc, gi, j0, g, kb);
                     const double a1 = vent(S.chunk, LD, li, rc, gi, j0, g + 8, kb);
@@ -385,7 +387,28 @@ __global__ void __launch_bounds__(kT, 1)
                     else if (q < ncol && li < rc) b = S.chunk[static_cast<size_t>(j0 + kt + q - KB) * LD + li];
                     else b = 0.0;
                     dmma(acc, a0, a1, b);
+                };
+                // k4 < kspec: rows gi < j0 + KB (unit triangle); k4 >= kfull: rows past rc.
+                // In between V is the stored column and every row exists: plain
+                // loads, two independent DMMA chains.
+                const int kspec = min(kb1, max(kb0, (j0 + KB - r_beg - lo + 3) >> 2));
+                const int kfull = max(kspec, min(kb1, (rc - lo) >> 2));
+                const double* pa0 = S.chunk + static_cast<size_t>(j0 + g) * LD + lo + t4;
+                const double* pa1 = pa0 + static_cast<size_t>(8) * LD;
+                const double* pb = S.chunk + static_cast<size_t>(q < KB ? j0 + q : j0 + kt + q - KB) * LD + lo + t4;
+                const bool za0 = g >= kb, za1 = g + 8 >= kb, zb = q >= ncol || (q < KB && q >= kb);
+                int k4 = kb0;
+                for (; k4 < kspec; ++k4) slow(k4);
+                for (; k4 + 1 < kfull; k4 += 2) {
+                    const int o = 4 * k4;
+                    const double a0 = za0 ? 0.0 : pa0[o], a1 = za1 ? 0.0 : pa1[o], b = zb ? 0.0 : pb[o];
+                    const double c0 = za0 ? 0.0 : pa0[o + 4], c1 = za1 ? 0.0 : pa1[o + 4], d = zb ? 0.0 : pb[o + 4];
+                    dmma(acc, a0, a1, b);
+                    dmma(acc2, c0, c1, d);
                 }
+                for (; k4 < kb1; ++k4) slow(k4);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[r] += acc2[r];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const int row = g + (r >= 2 ? 8 : 0), col = tile * 8 + 2 * t4 + (r & 1);
@@ -393,6 +416,7 @@ __global__ void __launch_bounds__(kT, 1)
                 }
             }
             __syncthreads();
+    if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 1] = clock64();
             // reduce over the K splits (fixed order) and scatter column slices to their owners
             const int ns = (ncol + CS - 1) / CS;
             for (int e = tid; e < KB * ncol; e += kT) {
@@ -406,6 +430,7 @@ __global__ void __launch_bounds__(kT, 1)
             }
             // owner: sum the CS partial slices in rank order and broadcast
             mbar_wait(&S.bar[2], static_cast<uint32_t>(phase & 1));
+    if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 2] = clock64();
             const int nxt = next_phase_j0(j0);
             if (tid == 0 && nxt >= 0) mbar_arm(&S.bar[2], rs_bytes(nxt));
             const int mine = max(0, min(ncol, (rank + 1) * ns) - rank * ns);
@@ -417,6 +442,7 @@ __global__ void __launch_bounds__(kT, 1)
                 for (int dst = 0; dst < CS; ++dst) st_async_f64(mapa_u32(off, dst), v, mapa_u32(bar0 + 24, dst));
             }
             mbar_wait(&S.bar[3], static_cast<uint32_t>(phase & 1));
+    if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 3] = clock64();
             if (tid == 0 && nxt >= 0) mbar_arm(&S.bar[3], ag_bytes(nxt));
             ++phase;
         }
@@ -437,6 +463,7 @@ __global__ void __launch_bounds__(kT, 1)
                 for (int c = 0; c < KB; ++c) S.tmat[lane * KB + c] = trow[c];
         }
         __syncthreads();
+        if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 4] = clock64();
         // Y = -T' Z in place (Z = zg[:, 16:])
         for (int k = tid; k < nrest; k += kT) {
             double z[KB];
@@ -451,6 +478,7 @@ __global__ void __launch_bounds__(kT, 1)
             }
         }
         __syncthreads();
+        if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 5] = clock64();
         // A_t += V Y over my rows >= j0: M = rows (tiles of 16), N = nrest (tiles of 8), K = 16
         {
             const int mt = (rc - lo + 15) >> 4, ntl = (nrest + 7) >> 3;
@@ -467,31 +495,49 @@ __global__ void __launch_bounds__(kT, 1)
                         const int li = r0 + g + 8 * h;
                         av[ks][h] = ks < nk ? vent(S.chunk, LD, li, rc, r_beg + li, j0, 4 * ks + t4, kb) : 0.0;
                     }
-                for (int tn = ng; tn < ntl; tn += ngr) {
-                    const int colb = tn * 8;
-                    double acc[4];
+                // two column tiles per iteration: both loaded before either is
+                // stored (a load after a store to the chunk cannot be hoisted),
+                // two independent DMMA chains
+                for (int tn = ng; tn < ntl; tn += 2 * ngr) {
+                    double acc[2][4];
+                    const int tn2 = tn + ngr;
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
-                        acc[r] = (li < rc && col < nrest) ? S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li] : 0.0;
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int colb = (h2 ? tn2 : tn) * 8;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
+                            acc[h2][r] = (li < rc && col < nrest && (h2 == 0 || tn2 < ntl))
+                                             ? S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li]
+                                             : 0.0;
+                        }
                     }
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
                         if (ks < nk) {
-                            const int yc = colb + g;
-                            const double b = yc < nrest ? S.zg[(4 * ks + t4) * ncol + KB + yc] : 0.0;
-                            dmma(acc, av[ks][0], av[ks][1], b);
+#pragma unroll
+                            for (int h2 = 0; h2 < 2; ++h2) {
+                                const int yc = (h2 ? tn2 : tn) * 8 + g;
+                                const double b = yc < nrest ? S.zg[(4 * ks + t4) * ncol + KB + yc] : 0.0;
+                                dmma(acc[h2], av[ks][0], av[ks][1], b);
+                            }
                         }
                     }
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
-                        if (li < rc && col < nrest) S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li] = acc[r];
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        if (h2 == 1 && tn2 >= ntl) break;
+                        const int colb = (h2 ? tn2 : tn) * 8;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
+                            if (li < rc && col < nrest) S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li] = acc[h2][r];
+                        }
                     }
                 }
             }
         }
         __syncthreads();
+        if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 6] = clock64();
     }
 
     for (int idx = tid; idx < w * rc; idx += kT) {
@@ -561,8 +607,8 @@ void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
     static const bool tracing = std::getenv("RUTV_QR_TRACE") != nullptr;  // debug: per-column clock64 trace
     long long* trace = nullptr;
     if (tracing) {
-        RUTV_CUDA(cudaMalloc(&trace, 64 * 8 * sizeof(long long)));
-        RUTV_CUDA(cudaMemset(trace, 0, 64 * 8 * sizeof(long long)));
+        RUTV_CUDA(cudaMalloc(&trace, 72 * 8 * sizeof(long long)));
+        RUTV_CUDA(cudaMemset(trace, 0, 72 * 8 * sizeof(long long)));
     }
     if (R <= kT)
         RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<1>, a.data, a.ld, s, w, p, R, LD, tau, trace));
@@ -570,7 +616,7 @@ void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
         RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<2>, a.data, a.ld, s, w, p, R, LD, tau, trace));
     note_launch();
     if (tracing) {
-        long long h[64 * 8];
+        long long h[72 * 8];
         RUTV_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
         cudaFree(trace);
         std::fprintf(stderr, "qr_reg trace s=%d w=%d cs=%d (cycles: wait, house, update, reduce, send, next)\n", s, w, cs);
@@ -579,6 +625,13 @@ void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
             std::fprintf(stderr, "  col %2d: %6lld %6lld %6lld %6lld %6lld %6lld\n", j, r[1] - r[0], r[2] - r[1],
                          r[3] - r[2], h[(j + 1) * 8 + 4] - r[3], h[(j + 1) * 8 + 5] - h[(j + 1) * 8 + 4],
                          h[(j + 1) * 8 + 0] - h[(j + 1) * 8 + 5]);
+        }
+        std::fprintf(stderr, "  block phases (cycles: partials, reduce-scatter, all-gather, T, Y, update)\n");
+        for (int ph = 0; ph < 8; ++ph) {
+            const long long* r = h + 64 * 8 + ph * 8;
+            if (!r[0]) break;
+            std::fprintf(stderr, "  phase %d: %6lld %6lld %6lld %6lld %6lld %6lld\n", ph, r[1] - r[0], r[2] - r[1],
+                         r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5]);
         }
     }
 }

@@ -100,12 +100,12 @@ const char* kPhaseNames[P_N] = {"start", "sketch", "qr_v", "apply_v", "qr_u", "a
 
 }  // namespace
 
-void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& fa) {
+void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArgs& fa) {
     const int64_t b = fa.b;
     configure_pool(device);
     Profiler prof;
     prof.on = std::getenv("RUTV_PROFILE") && std::strcmp(std::getenv("RUTV_PROFILE"), "0") != 0;
-    prof.st = st;
+    prof.st = st_in;
     prof.mark(P_START);
     gemm_profile_begin();
     const char* ov_env = std::getenv("RUTV_OVERLAP");
@@ -132,10 +132,25 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
     }
     const int nsteps = static_cast<int>(plan.size());
 
-    cudaStream_t sB = st, sC = st;
+    // Streams.  With overlap the critical chain runs on a HIGH-priority stream
+    // A (and its look-ahead helper C), the V/U accumulation on a low-priority
+    // stream B: when both have blocks waiting, the block scheduler hands free
+    // SMs to the critical chain first and B fills the rest (the panel QR
+    // kernels leave ~130 SMs idle).  Stream A first waits for the caller's
+    // stream (the input may still be in flight there); the call ends with a
+    // host synchronisation on A, so the results are complete on return.
+    cudaStream_t st = st_in, sB = st_in, sC = st_in;
     if (overlap) {
-        RUTV_CUDA(cudaStreamCreateWithFlags(&sB, cudaStreamNonBlocking));
-        RUTV_CUDA(cudaStreamCreateWithFlags(&sC, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;
+        RUTV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio_hi));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sC, cudaStreamNonBlocking, prio_hi));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, prio_lo));
+        cudaEvent_t e_in;
+        RUTV_CUDA(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
+        RUTV_CUDA(cudaEventRecord(e_in, st_in));
+        RUTV_CUDA(cudaStreamWaitEvent(st, e_in, 0));
+        cudaEventDestroy(e_in);
     }
     struct StreamGuard {
         cudaStream_t s;
@@ -143,7 +158,7 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
         ~StreamGuard() {
             if (own) cudaStreamDestroy(s);
         }
-    } sguard{sB, overlap}, sguardC{sC, overlap};
+    } sguardA{st, overlap}, sguard{sB, overlap}, sguardC{sC, overlap};
     std::vector<cudaEvent_t> events;
     struct EventGuard {
         std::vector<cudaEvent_t>& ev;
@@ -210,15 +225,16 @@ void factorize_device(cudaStream_t st, int device, int64_t n, const FactorArgs& 
     // declared after every buffer -> destroyed first: stream B drains before any
     // buffer is released (also on the exception path)
     struct JoinGuard {
-        cudaStream_t s, c;
+        cudaStream_t a, s, c;
         bool own;
         ~JoinGuard() {
             if (own) {
+                cudaStreamSynchronize(a);
                 cudaStreamSynchronize(s);
                 cudaStreamSynchronize(c);
             }
         }
-    } jguard{sB, sC, overlap};
+    } jguard{st, sB, sC, overlap};
 
     auto gemmA = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
                      const DView& c) { gemm(st, alpha, ta, a, tb, bm, beta, c, GWA.p, gw_elems); };
