@@ -49,8 +49,34 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def workload_name(n, b, q):
-    return f"config2: n={n} geometric sigma 1->1e-12, b={b}, q={q}, full U/T/V"
+# BASELINE.json configs (seeds fixed here: A from SEED_A, the sketch stream from SEED_G)
+CONFIGS = {
+    1: dict(n=2000, b=128, q=0, kind="gaussian"),
+    2: dict(n=4000, b=128, q=2, kind="geometric"),
+    3: dict(n=10000, b=256, q=1, kind="gaussian"),
+    4: dict(n=30000, b=256, q=2, kind="cliff"),
+    5: dict(n=50000, b=512, q=2, kind="gaussian"),
+}
+KIND_TEXT = {"gaussian": "iid N(0,1)", "geometric": "geometric sigma 1->1e-12 (Haar product)",
+             "cliff": "sigma=1 (i<=3000) then 1e-3*0.999^(i-3000) (Haar product)"}
+
+
+def workload_name(n, b, q, kind="geometric", cfg=2):
+    return f"config{cfg}: n={n} {KIND_TEXT[kind]}, b={b}, q={q}, full U/T/V"
+
+
+def make_matrix(rutv, a, kind, seed):
+    """A on the device with the reference's generators (metrics.cpp:90-110)."""
+    n = a.shape[0]
+    if kind == "gaussian":
+        rutv.gaussian_matrix_device(a, seed)
+    elif kind == "geometric":
+        rutv.spectrum_matrix_device(a, seed, beta=10 ** (-12 / (n - 1)))
+    else:
+        import numpy as np
+        i = np.arange(1, n + 1)
+        sig = np.where(i <= 3000, 1.0, 1e-3 * 0.999 ** (i - 3000.0))
+        rutv.spectrum_matrix_device(a, seed, sigma=sig)
 
 
 # ----------------------------------------------------------------- clocks --
@@ -152,7 +178,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * statistics.median(times), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(N_DEF, B_DEF, Q_DEF), "sample_n": n, "b": B_DEF,
+        "config": {"workload": workload_name(args.n, args.b, args.q, args.kind, args.config), "sample_n": n, "b": B_DEF,
                    "q": Q_DEF, "parallelism": "cpu-1thread"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": 1, "kind": kind,
                          "sample": sample},
@@ -174,13 +200,23 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEF)
-    ap.add_argument("--b", type=int, default=B_DEF)
-    ap.add_argument("--q", type=int, default=Q_DEF)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default 2, the single-GPU headline)")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--b", type=int, default=None)
+    ap.add_argument("--q", type=int, default=None)
+    ap.add_argument("--sharded", action="store_true",
+                    help="N > 1: ONE matrix on the 2D block-cyclic grid (dist.py, NCCL), strong scaling; "
+                         "default: one independent factorization per GPU (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    cfgd = CONFIGS[args.config]
+    args.n = cfgd["n"] if args.n is None else args.n
+    args.b = cfgd["b"] if args.b is None else args.b
+    args.q = cfgd["q"] if args.q is None else args.q
+    args.kind = cfgd["kind"]
     if args.impl == "reference":
         return run_reference(args)
 
@@ -197,9 +233,11 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     n, b, q = args.n, args.b, args.q
     F = rutv.flops(n, b, q)
+    if args.sharded:
+        return run_sharded(args, torch, dist, rutv, world, rank, local, dev, F)
 
     a = cm(torch, n, n, dev)
-    rutv.spectrum_matrix_device(a, SEED_A + rank, beta=10 ** (-12 / (n - 1)))
+    make_matrix(rutv, a, args.kind, SEED_A + rank)
     t, u, v = cm(torch, n, n, dev), cm(torch, n, n, dev), cm(torch, n, n, dev)
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
@@ -323,12 +361,101 @@ def main():
             "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device-generated Haar product, seed 1)",
-            "config": {"workload": workload_name(n, b, q), "n": n, "b": b, "q": q,
+            "data": f"synthetic (device-generated {KIND_TEXT[args.kind]}, seed {SEED_A})",
+            "config": {"workload": workload_name(n, b, q, args.kind, args.config), "n": n, "b": b, "q": q,
                        "flops_per_step": F, "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (A 128 MB + 384 MB state) exceed the 126 MB L2; no flush"},
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
             "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ---------------------------------------------------------- sharded (2D) --
+def run_sharded(args, torch, dist, rutv, world, rank, local, dev, F):
+    """ONE matrix on the P x Q block-cyclic grid (dist.py): strong scaling.
+    value = F / (max over ranks of the device time of one factorization)."""
+    from paper_2104_05782_b200.dist import CudaOps, Grid, factorize_dist, grid_shape, make_comms, scatter_grid
+    n, b, q = args.n, args.b, args.q
+    P, Q = grid_shape(world)
+    grid = Grid(n, b, P, Q, rank)
+    comms = make_comms(grid) if world > 1 else None
+    full = cm(torch, n, n, dev)
+    make_matrix(rutv, full, args.kind, SEED_A)  # same matrix on every rank (deterministic generator)
+    a_loc = scatter_grid(full, grid)
+    del full
+    torch.cuda.empty_cache()
+    ops = CudaOps(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(x):
+        return factorize_dist(x, grid, q=q, seed=SEED_G, ops=ops, comms=comms)
+
+    for _ in range(args.warmup):
+        step(a_loc)
+    torch.cuda.synchronize()
+    launches0 = rutv.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(a_loc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = rutv.launch_count() - launches0
+    ms_t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    # e2e: this rank's blocks from pinned host memory, results back to pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        mr, mc = a_loc.shape
+        ha = torch.empty((mc, mr), dtype=torch.float64, pin_memory=True).T
+        ha.copy_(a_loc)
+        hout = [torch.empty((mc, mr), dtype=torch.float64, pin_memory=True).T for _ in range(3)]
+        dbuf = torch.empty_like(a_loc)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            dbuf.copy_(ha, non_blocking=True)
+            t, u, v = step(dbuf)
+            for h, d in zip(hout, (t, u, v)):
+                h.copy_(d, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(F / (float(ems.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "ms_per_step": round(float(ems.item()), 3),
+               "h2d_bytes_per_step": 8 * mr * mc, "d2h_bytes_per_step": 3 * 8 * mr * mc, "per_rank": True}
+    if rank == 0:
+        value = F / (ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (device-generated {KIND_TEXT[args.kind]}, seed {SEED_A})",
+            "config": {"workload": workload_name(n, b, q, args.kind, args.config), "n": n, "b": b, "q": q,
+                       "flops_per_step": F, "parallelism": f"2d-block-cyclic {P}x{Q}",
+                       "l2": "state exceeds the 126 MB L2; no flush"},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "roofline": {"bound": "tensor", "achieved": round(value / 1e3 / world, 3), "peak": DMMA_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": round(value / 1e3 / world / DMMA_PEAK_TFLOPS, 4),
+                         "traffic": None, "kernel": "whole factorization per GPU (dist driver)"},
+            "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
