@@ -550,7 +550,9 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t work_elems) {
     }
     const int64_t tb = ((M + 127) / 128) * ((N + 63) / 64);
     if (K < 1024 && tb < slots) return {false, 1};  // small late-step updates: more, smaller tiles
-    if (tb >= 3 * slots || K < 1024) return {true, 1};
+    if (K < 1024 || (tb >= 3 * slots && K < 4096)) return {true, 1};
+    // long K: the wave model also fixes the quantisation of mid-size grids
+    // (e.g. 940 tiles = 3.2 waves of 296 at config 4's sketch)
     return {true, cap(choose_splits(M, N, K, tb, 128 * 64 * 2, slots, std::min<int64_t>(K / 256, 32)))};
 }
 
