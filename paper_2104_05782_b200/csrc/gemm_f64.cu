@@ -303,15 +303,82 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, (gemm_min_blocks<B
     }
 
 #pragma unroll
+    // Fast loads (16-byte path): every thread's chunk coordinates inside a tile
+    // are fixed, so the global pointers, shared offsets and the m/n-boundary
+    // byte counts are computed once; a full k-tile is then one pointer bump and
+    // one cp.async per chunk (the generic load_tile keeps the partial last tile).
+    constexpr int ACH = VEC ? (BK * BM / 2 + NT - 1) / NT : 1;
+    constexpr int BCH = VEC ? (BK * BN / 2 + NT - 1) / NT : 1;
+    const double* agp[ACH];
+    const double* bgp[BCH];
+    int aso[ACH], bso[BCH], aby[ACH], bby[BCH];
+    const int64_t astep = TA ? BK : BK * p.lda, bstep = TB ? BK * p.ldb : BK;
+    if constexpr (VEC) {
+#pragma unroll
+        for (int i = 0; i < ACH; ++i) {
+            const int c = tid + i * NT;
+            int mm, kk;
+            if constexpr (!TA) {
+                kk = c / (BM / 2);
+                mm = (c % (BM / 2)) * 2;
+                aso[i] = kk * G::A_LD + mm;
+            } else {
+                mm = c / (BK / 2);
+                kk = (c % (BK / 2)) * 2;
+                aso[i] = mm * G::A_LD + kk;
+            }
+            const int64_t gm = m0 + mm;
+            const bool ok = c < BK * BM / 2 && gm < M;
+            aby[i] = !ok ? 0 : (!TA && gm + 1 >= M ? 8 : 16);
+            agp[i] = ok ? (TA ? p.A + (kbeg + kk) + gm * p.lda : p.A + gm + (kbeg + kk) * p.lda) : p.A;
+            if (c >= BK * BM / 2) aso[i] = 0;
+        }
+#pragma unroll
+        for (int i = 0; i < BCH; ++i) {
+            const int c = tid + i * NT;
+            int nn, kk;
+            if constexpr (!TB) {
+                nn = c / (BK / 2);
+                kk = (c % (BK / 2)) * 2;
+                bso[i] = nn * G::B_LD + kk;
+            } else {
+                kk = c / (BN / 2);
+                nn = (c % (BN / 2)) * 2;
+                bso[i] = kk * G::B_LD + nn;
+            }
+            const int64_t gn = n0 + nn;
+            const bool ok = c < BK * BN / 2 && gn < N;
+            bby[i] = !ok ? 0 : (TB && gn + 1 >= N ? 8 : 16);
+            bgp[i] = ok ? (TB ? p.B + gn + (kbeg + kk) * p.ldb : p.B + (kbeg + kk) + gn * p.ldb) : p.B;
+            if (c >= BK * BN / 2) bso[i] = 0;
+        }
+    }
+    auto load = [&](int stage, int kt) {
+        const int64_t k0 = kbeg + static_cast<int64_t>(kt) * BK;
+        if (VEC && k0 + BK <= kend) {
+            double* as = As + stage * G::A_SZ;
+            double* bs = Bs + stage * G::B_SZ;
+#pragma unroll
+            for (int i = 0; i < ACH; ++i)
+                if (BK * BM / 2 % NT == 0 || tid + i * NT < BK * BM / 2)
+                    cp_async16(as + aso[i], aby[i] ? agp[i] + kt * astep : p.A, aby[i]);
+#pragma unroll
+            for (int i = 0; i < BCH; ++i)
+                if (BK * BN / 2 % NT == 0 || tid + i * NT < BK * BN / 2)
+                    cp_async16(bs + bso[i], bby[i] ? bgp[i] + kt * bstep : p.B, bby[i]);
+        } else {
+            load_tile(stage, k0);
+        }
+    };
     for (int s = 0; s < ST - 1; ++s) {
-        if (s < KT) load_tile(s, kbeg + static_cast<int64_t>(s) * BK);
+        if (s < KT) load(s, s);
         cp_async_commit();
     }
     for (int kt = 0; kt < KT; ++kt) {
         cp_async_wait<ST - 2>();
         __syncthreads();
         const int nk = kt + ST - 1;
-        if (nk < KT) load_tile(nk % ST, kbeg + static_cast<int64_t>(nk) * BK);
+        if (nk < KT) load(nk % ST, nk);
         cp_async_commit();
         const double* as = As + (kt % ST) * G::A_SZ;
         const double* bs = Bs + (kt % ST) * G::B_SZ;
