@@ -9,6 +9,18 @@ namespace rutv {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Explicit shared-state-space accesses by 32-bit address: pointers carried in
+// structs / lambda captures are generic to the compiler, and in a cluster
+// kernel every generic shared access re-derives the CTA's window (S2UR
+// SR_CgaCtaId + LEA per load); hot loops precompute addresses and use these.
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));

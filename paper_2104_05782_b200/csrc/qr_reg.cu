@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(kT, 1)
     cluster.sync();  // every CTA live, barriers initialised, before any remote traffic
 
     const uint32_t msg_a = smem_u32(S.msg);
+    const uint32_t part_a = smem_u32(S.part), hsend_a = smem_u32(S.hsend), chunk_a = smem_u32(S.chunk);
     const uint32_t bar0 = smem_u32(S.bar);  // mbarrier b at bar0 + 8 b
 
     // Reduce the 16 per-thread partial dots over the row-owning warps and
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kT, 1)
             }
         }
         const double v = vals[0] + __shfl_xor_sync(kFull, vals[0], 1);
-        if ((lane & 1) == 0) S.part[warp * KB + (lane >> 1)] = v;
+        if ((lane & 1) == 0) sts_f64(part_a + 8u * static_cast<uint32_t>(warp * KB + (lane >> 1)), v);
         asm volatile("bar.sync 1, %0;" ::"r"(nwact * 32) : "memory");
         if (trace && tid == 0 && rank == 0 && jn < 64) trace[jn * 8 + 4] = clock64();
         // every row-owning warp forms the (identical) message and sends it to
@@ -185,9 +186,9 @@ __global__ void __launch_bounds__(kT, 1)
         if (warp < CS) {
             double val = 0.0;
             if (lane < KB) {
-                for (int ww = 0; ww < nwact; ++ww) val += S.part[ww * KB + lane];
+                for (int ww = 0; ww < nwact; ++ww) val += lds_f64(part_a + 8u * static_cast<uint32_t>(ww * KB + lane));
             } else if (jn >= r_beg && jn < r_beg + rc) {
-                val = S.hsend[lane - KB];
+                val = lds_f64(hsend_a + 8u * static_cast<uint32_t>(lane - KB));
             }
             const int par = jn & 1;
             const uint32_t off = msg_a + static_cast<uint32_t>(((par * CS + rank) * kMsg + lane) * 8);
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kT, 1)
                         for (int k = 0; k < KB; ++k) vals[k] += x[m][0] * x[m][k];
                     } else if (li < rc && gi == j0) {
 #pragma unroll
-                        for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
+                        for (int k = 0; k < KB; ++k) sts_f64(hsend_a + 8u * k, x[m][k]);
                     }
                 }
                 col_send(vals, j0);
@@ -244,14 +245,14 @@ __global__ void __launch_bounds__(kT, 1)
                 if (tr) trace[j * 8 + 1] = clock64();
                 double tsum;
                 {
-                    const double* mp = S.msg + par * CS * kMsg + lane;
+                    const uint32_t mp = msg_a + 8u * static_cast<uint32_t>(par * CS * kMsg + lane);
                     double t0 = 0.0, t1 = 0.0;
                     int r = 0;
                     for (; r + 1 < CS; r += 2) {
-                        t0 += mp[r * kMsg];
-                        t1 += mp[(r + 1) * kMsg];
+                        t0 += lds_f64(mp + 8u * static_cast<uint32_t>(r * kMsg));
+                        t1 += lds_f64(mp + 8u * static_cast<uint32_t>((r + 1) * kMsg));
                     }
-                    if (r < CS) t0 += mp[r * kMsg];
+                    if (r < CS) t0 += lds_f64(mp + 8u * static_cast<uint32_t>(r * kMsg));
                     tsum = t0 + t1;
                 }
                 // house() (householder.cpp:20-34); 1/head and 1/beta by reciprocals
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
                 for (int m = 0; m < MR; ++m) {
                     const int li = tid + kT * m;
-                    if (li < rc) S.chunk[static_cast<size_t>(j) * LD + li] = x[m][0];
+                    if (li < rc) sts_f64(chunk_a + 8u * static_cast<uint32_t>(j * LD + li), x[m][0]);
 #pragma unroll
                     for (int k = 0; k + 1 < KB; ++k) x[m][k] = x[m][k + 1];
                     x[m][KB - 1] = 0.0;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kT, 1)
                         const int li = tid + kT * m, gi = r_beg + li;
                         if (li < rc && gi == jn) {
 #pragma unroll
-                            for (int k = 0; k < KB; ++k) S.hsend[k] = x[m][k];
+                            for (int k = 0; k < KB; ++k) sts_f64(hsend_a + 8u * k, x[m][k]);
                         }
                     }
                     col_send(vals, jn);
@@ -393,18 +394,21 @@ __global__ void __launch_bounds__(kT, 1)
                 // loads, two independent DMMA chains.
                 const int kspec = min(kb1, max(kb0, (j0 + KB - r_beg - lo + 3) >> 2));
                 const int kfull = max(kspec, min(kb1, (rc - lo) >> 2));
-                const double* pa0 = S.chunk + static_cast<size_t>(j0 + g) * LD + lo + t4;
-                const double* pa1 = pa0 + static_cast<size_t>(8) * LD;
-                const double* pb = S.chunk + static_cast<size_t>(q < KB ? j0 + q : j0 + kt + q - KB) * LD + lo + t4;
                 const bool za0 = g >= kb, za1 = g + 8 >= kb, zb = q >= ncol || (q < KB && q >= kb);
+                // masked operands read a valid clamped column (column j0) and are zeroed by select
+                const uint32_t cbase = smem_u32(S.chunk) + 8u * static_cast<uint32_t>(lo + t4);
+                const uint32_t pa0 = cbase + 8u * static_cast<uint32_t>((za0 ? j0 : j0 + g) * LD);
+                const uint32_t pa1 = cbase + 8u * static_cast<uint32_t>((za1 ? j0 : j0 + g + 8) * LD);
+                const uint32_t pb =
+                    cbase + 8u * static_cast<uint32_t>((zb ? j0 : (q < KB ? j0 + q : j0 + kt + q - KB)) * LD);
                 int k4 = kb0;
                 for (; k4 < kspec; ++k4) slow(k4);
                 for (; k4 + 1 < kfull; k4 += 2) {
-                    const int o = 4 * k4;
-                    const double a0 = za0 ? 0.0 : pa0[o], a1 = za1 ? 0.0 : pa1[o], b = zb ? 0.0 : pb[o];
-                    const double c0 = za0 ? 0.0 : pa0[o + 4], c1 = za1 ? 0.0 : pa1[o + 4], d = zb ? 0.0 : pb[o + 4];
-                    dmma(acc, a0, a1, b);
-                    dmma(acc2, c0, c1, d);
+                    const uint32_t o = 32u * static_cast<uint32_t>(k4);
+                    const double a0r = lds_f64(pa0 + o), a1r = lds_f64(pa1 + o), br = lds_f64(pb + o);
+                    const double c0r = lds_f64(pa0 + o + 32), c1r = lds_f64(pa1 + o + 32), dr = lds_f64(pb + o + 32);
+                    dmma(acc, za0 ? 0.0 : a0r, za1 ? 0.0 : a1r, zb ? 0.0 : br);
+                    dmma(acc2, za0 ? 0.0 : c0r, za1 ? 0.0 : c1r, zb ? 0.0 : dr);
                 }
                 for (; k4 < kb1; ++k4) slow(k4);
 #pragma unroll
@@ -498,8 +502,11 @@ __global__ void __launch_bounds__(kT, 1)
                 // two column tiles per iteration: both loaded before either is
                 // stored (a load after a store to the chunk cannot be hoisted),
                 // two independent DMMA chains
+                const uint32_t cb = smem_u32(S.chunk), zb0 = smem_u32(S.zg);
                 for (int tn = ng; tn < ntl; tn += 2 * ngr) {
                     double acc[2][4];
+                    uint32_t ad[2][4];
+                    bool ok[2][4];
                     const int tn2 = tn + ngr;
 #pragma unroll
                     for (int h2 = 0; h2 < 2; ++h2) {
@@ -507,9 +514,10 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
-                            acc[h2][r] = (li < rc && col < nrest && (h2 == 0 || tn2 < ntl))
-                                             ? S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li]
-                                             : 0.0;
+                            ok[h2][r] = li < rc && col < nrest && (h2 == 0 || tn2 < ntl);
+                            ad[h2][r] = ok[h2][r] ? cb + 8u * static_cast<uint32_t>((j0 + kt + col) * LD + li) : cb;
+                            const double v = lds_f64(ad[h2][r]);
+                            acc[h2][r] = ok[h2][r] ? v : 0.0;
                         }
                     }
 #pragma unroll
@@ -518,21 +526,18 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
                             for (int h2 = 0; h2 < 2; ++h2) {
                                 const int yc = (h2 ? tn2 : tn) * 8 + g;
-                                const double b = yc < nrest ? S.zg[(4 * ks + t4) * ncol + KB + yc] : 0.0;
-                                dmma(acc[h2], av[ks][0], av[ks][1], b);
+                                const bool yok = yc < nrest;
+                                const double bv = lds_f64(
+                                    zb0 + 8u * static_cast<uint32_t>((4 * ks + t4) * ncol + KB + (yok ? yc : 0)));
+                                dmma(acc[h2], av[ks][0], av[ks][1], yok ? bv : 0.0);
                             }
                         }
                     }
 #pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        if (h2 == 1 && tn2 >= ntl) break;
-                        const int colb = (h2 ? tn2 : tn) * 8;
+                    for (int h2 = 0; h2 < 2; ++h2)
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int li = r0 + g + (r >= 2 ? 8 : 0), col = colb + 2 * t4 + (r & 1);
-                            if (li < rc && col < nrest) S.chunk[static_cast<size_t>(j0 + kt + col) * LD + li] = acc[h2][r];
-                        }
-                    }
+                        for (int r = 0; r < 4; ++r)
+                            if (ok[h2][r]) sts_f64(ad[h2][r], acc[h2][r]);
                 }
             }
         }
