@@ -191,6 +191,12 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
     const int64_t sb = std::max<int64_t>(n * bb, 1);
     // stream A private
     DevBuf G(fa.dG ? 1 : sb, st), Y(sb, st), Z(sb, st), ZxA(std::max<int64_t>((vr + n) * bb, 1), st);
+    // sketch hoisting (see the step loop): the next step's G and Y, H = M_u(b:, :)' G
+    DevBuf G2(fa.dG ? 1 : sb, st), Y2(sb, st), Hh(bb * bb, st);
+    double* Gb[2] = {G.p, G2.p};
+    double* Yb[2] = {Y.p, Y2.p};
+    const char* hoist_env = std::getenv("RUTV_HOIST");
+    const bool hoist = !(hoist_env && std::strcmp(hoist_env, "0") == 0);
     DevBuf ZlA(sb, st), Twy(bb * bb, st), Gram(bb * bb, st), tau(bb + 1, st);
     // double-buffered A -> B hand-off
     DevBuf Wv0(sb, st), Wv1(sb, st), Mv0(sb, st), Mv1(sb, st);
@@ -252,6 +258,7 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
     };
 
     uint64_t pos = 0;  // stream position P_i
+    bool have_y = false;  // Y of this step formed by the previous one
     std::vector<cudaEvent_t> evB;
     for (int i = 0; i < nsteps; ++i) {
         const int64_t r0 = plan[static_cast<size_t>(i)].r0, s = plan[static_cast<size_t>(i)].s;
@@ -263,13 +270,18 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         }
         const int par = i & 1;
         if (i >= 2) wait(st, evB[static_cast<size_t>(i - 2)]);  // slot `par` free again
+        const bool hoist_next = hoist && i + 1 < nsteps && !plan[static_cast<size_t>(i + 1)].tail;
 
-        // ---- sketch (build_v_alpha, randutv_blocked.cpp:41-50)
-        DView Gv(s, b, s, fa.dG ? const_cast<double*>(fa.dG) + pos : G.p);
-        if (!fa.dG) normal_fill(st, fa.seed, pos, Gv);
+        // ---- sketch (build_v_alpha, randutv_blocked.cpp:41-50).  Y = T22' G was
+        // already formed during the previous step when it was hoisted (below).
+        DView Yv(s, b, s, Yb[par]), Zv(s, b, s, Z.p);
+        if (!have_y) {
+            DView Gv(s, b, s, fa.dG ? const_cast<double*>(fa.dG) + pos : Gb[par]);
+            if (!fa.dG) normal_fill(st, fa.seed, pos, Gv);
+            gemmA(1.0, Op::T, t22, Op::N, Gv, 0.0, Yv);
+        }
+        have_y = false;
         pos += static_cast<uint64_t>(s * b);
-        DView Yv(s, b, s, Y.p), Zv(s, b, s, Z.p);
-        gemmA(1.0, Op::T, t22, Op::N, Gv, 0.0, Yv);
         for (int it = 0; it < fa.q; ++it) {
             gemmA(1.0, Op::N, t22, Op::N, Yv, 0.0, Zv);
             gemmA(1.0, Op::T, t22, Op::N, Zv, 0.0, Yv);
@@ -293,6 +305,19 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
             wait(sC, record(st));
             gemm(sC, -1.0, Op::N, Zx, Op::T, DView(s - b, b, s, Mv[par] + b), 1.0, X.block(0, b, s, s - b),
                  GWC.p, gw_elems);
+            // Sketch hoisting.  The next trailing matrix is T22' = B(b:, :) - M_u(b:, :) Zl
+            // with B = (T22 Q_v)(:, b:) -- final right here -- and Zl = W_u' B, so
+            //   Y' = T22'^T G' = B(b:, :)^T G' - Zl^T (M_u(b:, :)^T G').
+            // The big product P = B(b:, :)^T G' runs now on stream C, on the SMs
+            // the panel QR leaves idle; the b-wide correction follows Q_u' on A.
+            // Mathematically the reference's Y = T22'^T G (randutv_blocked.cpp:45).
+            if (hoist_next) {
+                const int64_t s2 = s - b;
+                DView G2v(s2, b, s2, fa.dG ? const_cast<double*>(fa.dG) + pos : Gb[par ^ 1]);
+                if (!fa.dG) normal_fill(sC, fa.seed, pos, G2v);
+                gemm(sC, 1.0, Op::T, X.block(b, b, s2, s2), Op::N, G2v, 0.0, DView(s2, b, s2, Yb[par ^ 1]), GWC.p,
+                     gw_elems);
+            }
             evR = record(sC);
         }
         prof.mark(P_APPLYV);
@@ -309,6 +334,14 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
             DView Zl(b, s - b, b, ZlA.p);
             gemmA(1.0, Op::T, WuV, Op::N, B, 0.0, Zl);
             gemmA(-1.0, Op::N, MuV, Op::N, Zl, 1.0, B);
+            if (hoist_next) {  // Y' = P - Zl^T (M_u(b:, :)^T G')
+                const int64_t s2 = s - b;
+                DView G2v(s2, b, s2, fa.dG ? const_cast<double*>(fa.dG) + pos : Gb[par ^ 1]);
+                DView H(b, b, b, Hh.p);
+                gemmA(1.0, Op::T, MuV.block(b, 0, s2, b), Op::N, G2v, 0.0, H);
+                gemmA(-1.0, Op::T, DView(b, s2, b, ZlA.p), Op::N, H, 1.0, DView(s2, b, s2, Yb[par ^ 1]));
+                have_y = true;
+            }
         }
         const cudaEvent_t evU = record(st);
         prof.mark(P_APPLYU);
