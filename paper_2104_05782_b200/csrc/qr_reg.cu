@@ -105,6 +105,11 @@ __device__ __forceinline__ double vent(const double* chunk, int LD, int li, int 
     return gi == j ? 1.0 : 0.0;
 }
 
+// Debug ablation mask (RUTV_QR_ABLATE, timing experiments only -- results are
+// wrong when set): 1 = skip block phases, 2 = trivial house(), 4 = skip the
+// warp butterfly.
+__device__ int g_qr_ablate = 0;
+
 template <int MR>
 __global__ void __launch_bounds__(kT, 1)
     hqr_reg_kernel(double* A, int64_t lda, int s, int w, int p, int R, int LD, double* tau, long long* trace) {
@@ -164,10 +169,12 @@ __global__ void __launch_bounds__(kT, 1)
     // Reduce the 16 per-thread partial dots over the row-owning warps and
     // all-gather them, with the head row of column jn, to every CTA's message
     // slot jn & 1.  Called by the nwact row-owning warps only (named barrier).
+    const int ablate = g_qr_ablate;
     auto col_send = [&](double (&vals)[KB], int jn) {
         // butterfly reduce-scatter: after it lane l holds the sum of index l >> 1
 #pragma unroll
         for (int lvl = 0; lvl < 4; ++lvl) {
+            if (ablate & 4) break;
             const int o = 16 >> lvl, n = (KB / 2) >> lvl;
             const bool up = (lane & o) != 0;
 #pragma unroll
@@ -261,7 +268,11 @@ __global__ void __launch_bounds__(kT, 1)
                 const double hk = __shfl_sync(kFull, tsum, (lane + KB) & 31);  // lane k < 16: a(j, j+k)
                 double beta, tj, rh = 1.0;
                 bool scale = false;
-                if (sigma == 0.0) {
+                if (ablate & 2) {
+                    beta = alpha;
+                    tj = 1.0;
+                    scale = true;
+                } else if (sigma == 0.0) {
                     if (alpha >= 0.0) {
                         beta = alpha;
                         tj = 0.0;
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(kT, 1)
             }
         }
         __syncthreads();
-        if (j0 + kt >= w) continue;
+        if (j0 + kt >= w || (ablate & 1)) continue;
 
         const int tph = phase;
         if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 0] = clock64();
@@ -610,6 +621,13 @@ void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     static const bool tracing = std::getenv("RUTV_QR_TRACE") != nullptr;  // debug: per-column clock64 trace
+    static const int ablate = [] {
+        const char* e = std::getenv("RUTV_QR_ABLATE");
+        const int v = e ? std::atoi(e) : 0;
+        if (v) RUTV_CUDA(cudaMemcpyToSymbol(g_qr_ablate, &v, sizeof(int)));
+        return v;
+    }();
+    (void)ablate;
     long long* trace = nullptr;
     if (tracing) {
         RUTV_CUDA(cudaMalloc(&trace, 72 * 8 * sizeof(long long)));
