@@ -94,9 +94,9 @@ struct Profiler {
 
 thread_local std::vector<double> t_prof_ms;
 
-enum Phase { P_START, P_SKETCH, P_QRV, P_APPLYV, P_QRU, P_APPLYU, P_SVD, P_BETA, P_FINAL, P_N };
+enum Phase { P_START, P_SKETCH, P_QRV, P_APPLYV, P_QRU, P_APPLYU, P_SVD, P_BETA, P_FINAL, P_WYV, P_WYU, P_N };
 const char* kPhaseNames[P_N] = {"start", "sketch", "qr_v", "apply_v", "qr_u", "apply_u",
-                                "svd", "beta", "final"};
+                                "svd", "beta", "final", "wy_v", "wy_u"};
 
 }  // namespace
 
@@ -109,7 +109,10 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
     prof.mark(P_START);
     gemm_profile_begin();
     const char* ov_env = std::getenv("RUTV_OVERLAP");
-    const bool overlap = fa.overlap && !prof.on && !(ov_env && std::strcmp(ov_env, "0") == 0);
+    // RUTV_PROFILE=1: phase times with the streams serialised; =2: phase times of
+    // the critical stream with the overlap kept (a timeline of the real schedule)
+    const bool prof_overlap = prof.on && std::strcmp(std::getenv("RUTV_PROFILE"), "2") == 0;
+    const bool overlap = fa.overlap && (!prof.on || prof_overlap) && !(ov_env && std::strcmp(ov_env, "0") == 0);
 
     const bool bu = fa.build_u, bv = fa.build_v;
     const int64_t vr = bv ? n : 0;  // V rows on top of T in VT
@@ -159,6 +162,10 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
             if (own) cudaStreamDestroy(s);
         }
     } sguardA{st, overlap}, sguard{sB, overlap}, sguardC{sC, overlap};
+    if (prof_overlap) {  // re-anchor the timeline on the critical stream
+        prof.st = st;
+        prof.mark(P_START);
+    }
     std::vector<cudaEvent_t> events;
     struct EventGuard {
         std::vector<cudaEvent_t>& ev;
@@ -289,9 +296,10 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         prof.mark(P_SKETCH);
         // ---- V-side QR (:52-53)
         hqr_panel(st, Yv, tau.p, nullptr, 0, HQ.p, hqw);
+        prof.mark(P_QRV);
         form_wy(Yv, b, Wv[par], Mv[par]);
         const cudaEvent_t evV = record(st);
-        prof.mark(P_QRV);
+        prof.mark(P_WYV);
         DView WvV(s, b, s, Wv[par]), MvV(s, b, s, Mv[par]);
         cudaEvent_t evR = nullptr;
         {  // V-apply, critical rows: T22 (:140).  Panel-first look-ahead: the
@@ -324,9 +332,10 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
         DView panel = t22.block(0, 0, s, b);
         hqr_panel(st, panel, tau.p, nullptr, 0, HQ.p, hqw);
+        prof.mark(P_QRU);
         form_wy(panel, b, Wu[par], Mu[par]);
         copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
-        prof.mark(P_QRU);
+        prof.mark(P_WYU);
         DView WuV(s, b, s, Wu[par]), MuV(s, b, s, Mu[par]);
         wait(st, evR);
         {  // Q_u' on T22(:, b:) (:147)

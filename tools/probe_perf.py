@@ -26,6 +26,10 @@ def run(n, b, q, reps=int(os.environ.get('REPS', '3')), profile=os.environ.get('
         rutv.factorize_device(a, t, u, v, b=b, q=q, seed=2)
         os.environ["RUTV_PROFILE"] = "0"
         out["phases_ms"] = {k: round(v, 3) for k, v in rutv.last_profile().items()}
+        os.environ["RUTV_PROFILE"] = "2"  # critical-stream timeline with the overlap kept
+        rutv.factorize_device(a, t, u, v, b=b, q=q, seed=2)
+        os.environ["RUTV_PROFILE"] = "0"
+        out["critical_ms"] = {k: round(v, 3) for k, v in rutv.last_profile().items()}
     print(json.dumps(out), flush=True)
 
 for spec in sys.argv[1:]:
