@@ -180,6 +180,7 @@ class Comms:
     row: Comm
     col: Comm
     world: Comm
+    row_side: Comm | None = None  # a second row communicator for the off-critical stream
     _all: list = field(default_factory=list)
 
 
@@ -197,9 +198,13 @@ def make_comms(grid: Grid) -> Comms:
             return Comm(ranks, None)
         return Comm(ranks, dist.new_group(ranks))
 
+    def mk_side(ranks):  # always a separate group: its own NCCL stream, no coupling to the critical one
+        return Comm(ranks, dist.new_group(ranks)) if len(ranks) > 1 else Comm(ranks, None)
+
     rows = [mk(grid.row_ranks(pr)) for pr in range(grid.P)]
     cols = [mk(grid.col_ranks(pc)) for pc in range(grid.Q)]
-    return Comms(rows[grid.pr], cols[grid.pc], world, rows + cols)
+    sides = [mk_side(grid.row_ranks(pr)) for pr in range(grid.P)]
+    return Comms(rows[grid.pr], cols[grid.pc], world, sides[grid.pr], rows + cols + sides)
 
 
 def cm_empty(rows: int, cols: int, like: torch.Tensor | None = None, device=None) -> torch.Tensor:
@@ -256,6 +261,9 @@ def factorize_dist(a_loc: torch.Tensor, grid: Grid, *, q: int, seed: int, ops, b
         raise ValueError("block size must be >= 1 and q >= 0")
     if comms is None:
         comms = make_comms(grid)
+    if comms.row_side is None:
+        comms.row_side = comms.row
+    ops.begin()
     RA, CA = grid.rows, grid.cols
     mr, mc = grid.local_shape()
     if tuple(a_loc.shape) != (mr, mc):
@@ -319,16 +327,25 @@ def factorize_dist(a_loc: torch.Tensor, grid: Grid, *, q: int, seed: int, ops, b
         Y = _gather_blocks(ops, comms.row, CA, pc_of, Y_loc, i, s, b, a_loc)
         tau_v = ops.hqr(Y)
         Wv, Mv = ops.form_wy(Y, tau_v, b)
-        # ---- V-apply on [V; T](:, r0:) (:140-143): Zx = X_loc W_v[my cols] over the row comm
-        X = VT[:, ci:]
-        Zx = cm_empty(vr + mr, b, like=a_loc)
+        # ---- V-apply on [V; T](:, r0:) (:140-143): Zx = X_loc W_v[my cols] over the row comm.
+        # The rows of T22 are the critical chain; V and the finished rows of T
+        # (rows [0, vr + ri)) go to the side stream with their own row communicator.
+        Wl = Ml = None
         if m_c:
             Wl, Ml = _pick_rows(ops, Wv, CA, i, s, b), _pick_rows(ops, Mv, CA, i, s, b)
-            ops.gemm(1.0, 0, X, 0, Wl, 0.0, Zx)
-        if vr + mr:
-            _all_reduce(ops, Zx, comms.row)
-            if m_c:
-                ops.gemm(-1.0, 0, Zx, 1, Ml, 1.0, X)
+        for crit in (True, False):
+            X = VT[vr + ri:, ci:] if crit else VT[:vr + ri, ci:]
+            if X.shape[0] == 0:
+                continue
+            with ops.side(not crit):
+                if m_c:
+                    ops.keep(Wl, Ml)
+                Zx = cm_empty(X.shape[0], b, like=a_loc)
+                if m_c:
+                    ops.gemm(1.0, 0, X, 0, Wl, 0.0, Zx)
+                _all_reduce(ops, Zx, comms.row if crit else comms.row_side)
+                if m_c:
+                    ops.gemm(-1.0, 0, Zx, 1, Ml, 1.0, X)
         # ---- U-side panel QR (build_u_alpha, :58-64): block column i gathered in its
         #      process column, factored by the diagonal owner, broadcast to all
         pan_pc = i % Q
@@ -356,18 +373,23 @@ def factorize_dist(a_loc: torch.Tensor, grid: Grid, *, q: int, seed: int, ops, b
             _all_reduce(ops, Zl, comms.col)
             if m_r:
                 ops.gemm(-1.0, 0, Mr, 0, Zl, 1.0, Bc)
-        # ---- U accumulate (:148): like the V-apply, over the row comm
+        # ---- U accumulate (:148): like the V-apply, off the critical chain
         if build_uv and mr:
             Xu = U[:, ci:]
-            Zu = cm_empty(mr, b, like=a_loc)
             if m_c:
                 Wl, Ml = _pick_rows(ops, Wu, CA, i, s, b), _pick_rows(ops, Mu, CA, i, s, b)
-                ops.gemm(1.0, 0, Xu, 0, Wl, 0.0, Zu)
-            _all_reduce(ops, Zu, comms.row)
-            if m_c:
-                ops.gemm(-1.0, 0, Zu, 1, Ml, 1.0, Xu)
+            with ops.side(True):
+                if m_c:
+                    ops.keep(Wl, Ml)
+                Zu = cm_empty(mr, b, like=a_loc)
+                if m_c:
+                    ops.gemm(1.0, 0, Xu, 0, Wl, 0.0, Zu)
+                _all_reduce(ops, Zu, comms.row_side)
+                if m_c:
+                    ops.gemm(-1.0, 0, Zu, 1, Ml, 1.0, Xu)
 
     # ======== deferred beta stage (:66-82, :129-137, :150-154) ========
+    ops.join()
     mine = sorted(saved)
     res = ops.svd_batch([saved[k][0] for k in mine])     # [(Us, sigma, Vs)]
     fac = {k: r for k, r in zip(mine, res)}
@@ -486,9 +508,50 @@ class CudaOps:
         from . import lib
         self.L = lib()
         self.dev = device
-        self.stream = torch.cuda.current_stream(device)
-        self.L.rutv_b200_set_stream(C.c_uint64(self.stream.cuda_stream))
+        self.caller = torch.cuda.current_stream(device)
+        # critical chain on a high-priority stream, V/U accumulation on a
+        # low-priority one (the single-GPU driver's schedule, randutv.cu)
+        self.sA = torch.cuda.Stream(device, priority=-1)
+        self.sB = torch.cuda.Stream(device, priority=0)
+        self.stream = self.caller
+        self._set(self.caller)
         self.status: list[torch.Tensor] = []
+
+    def _set(self, st):
+        self.stream = st
+        torch.cuda.set_stream(st)
+        self.L.rutv_b200_set_stream(C.c_uint64(st.cuda_stream))
+
+    # stream schedule
+    def begin(self):
+        self.caller = torch.cuda.current_stream(self.dev)
+        self.sA.wait_stream(self.caller)
+        self._set(self.sA)
+
+    def side(self, on: bool = True):
+        ops = self
+
+        class _Side:
+            def __enter__(self_):
+                if on:
+                    ops.sB.wait_stream(ops.sA)
+                    ops._set(ops.sB)
+
+            def __exit__(self_, *exc):
+                if on:
+                    ops._set(ops.sA)
+                return False
+        return _Side()
+
+    def keep(self, *tensors):
+        """Tensors made on the critical stream and read on the side stream."""
+        if self.stream is self.sB:
+            for t in tensors:
+                if t is not None:
+                    t.record_stream(self.sB)
+
+    def join(self):
+        self.sA.wait_stream(self.sB)
 
     # helpers
     @staticmethod
@@ -603,6 +666,9 @@ class CudaOps:
 
     def finish(self):
         from . import ConvergenceError
+        self.join()
+        self.caller.wait_stream(self.sA)
+        self._set(self.caller)
         torch.cuda.synchronize(self.dev)
         for st in self.status:
             h = st.cpu().view(-1, 4)

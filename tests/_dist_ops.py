@@ -17,7 +17,26 @@ def _np(x):
     return np.asfortranarray(x.detach().numpy())
 
 
+class _NoSide:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 class TorchCpuOps:
+    def begin(self):
+        pass
+
+    def side(self, on=True):
+        return _NoSide()
+
+    def keep(self, *tensors):
+        pass
+
+    def join(self):
+        pass
     def copy(self, dst, src):
         dst.copy_(src)
 
