@@ -138,13 +138,41 @@ class ClockSampler:
 
 # -------------------------------------------------------------- reference --
 def reference_sample(n=1000, b=B_DEF, q=Q_DEF):
-    """Time the unmodified reference randutv() (oracle/_ref) once on the sample."""
+    """Time the unmodified reference randutv() (oracle/_ref) once on the sample (1 thread)."""
     import oracle
     a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A, impl="ref")
     t0 = time.perf_counter()
     oracle.randutv(a, b=b, q=q, seed=SEED_G, impl="ref")
     dt = time.perf_counter() - t0
     return oracle.flops(n, b, q) / dt / 1e9, dt
+
+
+def reference_ab_sample(n=1024, b=B_DEF, q=Q_DEF, workers=None):
+    """The reference's multi-threaded algorithm-by-blocks driver (randutv_ab, every host
+    thread) on the same family; it needs b | n, hence n = 1024 (8 x 128)."""
+    import oracle
+    workers = workers or os.cpu_count() or 1
+    a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A, impl="ref")
+    t0 = time.perf_counter()
+    oracle.ref_randutv_ab(a, b=b, q=q, seed=SEED_G, workers=workers)
+    dt = time.perf_counter() - t0
+    return oracle.flops(n, b, q) / dt / 1e9, dt, workers
+
+
+def best_reference():
+    """The faster of the reference's two CPU drivers on the box's host cores:
+    (value GFLOP/s, seconds, cores, sample text)."""
+    v1, dt1 = reference_sample(1000)
+    try:
+        v2, dt2, w = reference_ab_sample(1024)
+    except Exception:  # the AB driver is an extra; the blocked one always exists
+        v2, dt2, w = -1.0, 0.0, 1
+    if v2 > v1:
+        return v2, dt2, w, (f"reference randutv_ab (algorithm-by-blocks, {w} threads) on n=1024 of the config-2 "
+                            f"family (b=128, q=2, geometric), {dt2:.2f} s; single-thread blocked randutv() on "
+                            f"n=1000: {v1:.2f} GFLOP/s")
+    return v1, dt1, 1, (f"reference randutv() (blocked, single thread by contract) on n=1000 of the config-2 "
+                        f"family (b=128, q=2, geometric), {dt1:.2f} s")
 
 
 def run_reference(args):
@@ -156,31 +184,31 @@ def run_reference(args):
         kind = "port"
     else:
         kind = "reference"
-    n = 1000
-    vals, times = [], []
+    vals, times, cores, sample = [], [], 1, ""
     for i in range(args.warmup + args.steps):
         if kind == "reference":
-            v, dt = reference_sample(n)
+            v, dt, cores, sample = best_reference()
         else:  # the C restatement (only if the reference library is missing)
+            n = 1000
             a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A)
             t0 = time.perf_counter()
             oracle.randutv(a, b=B_DEF, q=Q_DEF, seed=SEED_G)
             dt = time.perf_counter() - t0
             v = oracle.flops(n, B_DEF, Q_DEF) / dt / 1e9
+            sample = f"C restatement of randutv() on n={n}, single thread"
         if i >= args.warmup:
             vals.append(v)
             times.append(dt)
     value = statistics.median(vals)
-    sample = (f"full factorization of an n={n} member of the config-2 family (b=128, q=2, geometric "
-              f"sigma 1->1e-12), reference randutv() single thread; value = F({n},128,2)/t")
+    sample += "; value = F(n,128,2)/t, median over the timed steps"
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * statistics.median(times), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.n, args.b, args.q, args.kind, args.config), "sample_n": n, "b": B_DEF,
-                   "q": Q_DEF, "parallelism": "cpu-1thread"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": 1, "kind": kind,
+        "config": {"workload": workload_name(args.n, args.b, args.q, args.kind, args.config), "b": B_DEF,
+                   "q": Q_DEF, "parallelism": f"cpu-{cores}threads"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -348,10 +376,9 @@ def main():
         try:
             import oracle
             if oracle.available("ref"):
-                v_ref, dt = reference_sample(1000)
-                cpu = {"value": round(v_ref, 4), "unit": "GFLOP/s", "cores": 1, "kind": "reference",
-                       "sample": f"reference randutv() on n=1000 of the config-2 family "
-                                 f"(b=128, q=2, geometric), {dt:.2f} s, single thread"}
+                v_ref, dt, cores, sample = best_reference()
+                cpu = {"value": round(v_ref, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                       "sample": sample}
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {exc}"}

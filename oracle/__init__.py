@@ -377,3 +377,17 @@ def ref_lowrank_error(a, t, u, v, k: int, norm: str = "fro") -> float:
     if rc != 0:
         raise OracleError(rc)
     return out.value
+
+
+def ref_randutv_ab(a, *, b: int, q: int, seed: int, workers: int):
+    """The reference's algorithm-by-blocks driver (randutv_ab.hpp:46) on `workers` threads."""
+    a = _f(a)
+    m, n = a.shape
+    L = _lib("ref")
+    L.ref_randutv_ab.argtypes = [_D, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64, C.c_int, _D, _D, _D, _D]
+    t, u, v = np.zeros((m, n), order="F"), np.zeros((m, m), order="F"), np.zeros((n, n), order="F")
+    res = C.c_double(0.0)
+    rc = L.ref_randutv_ab(_p(a), m, n, max(m, 1), b, q, seed, workers, _p(t), _p(u), _p(v), C.byref(res))
+    if rc != 0:
+        raise OracleError(rc, res.value)
+    return t, u, v

@@ -25,6 +25,7 @@
 #include "randutv/matrix_io.hpp"
 #include "randutv/matrix_ops.hpp"
 #include "randutv/metrics.hpp"
+#include "randutv/randutv_ab.hpp"
 #include "randutv/randutv_blocked.hpp"
 #include "randutv/rng.hpp"
 
@@ -222,6 +223,25 @@ int ref_gemm(double alpha, int ta, const double* a, int64_t ar, int64_t ac, int6
         return 0;
     } catch (...) {
         return status_of(std::current_exception(), nullptr);
+    }
+}
+
+// The reference's multi-threaded algorithm-by-blocks driver (randutv_ab.hpp:46):
+// timed as the CPU baseline with every host thread (b must divide m and n).
+int ref_randutv_ab(const double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int q, uint64_t seed,
+                   int workers, double* t, double* u, double* v, double* residual) {
+    try {
+        UTVConfig cfg;
+        cfg.b = b;
+        cfg.q = q;
+        cfg.seed = seed;
+        UTVResult r = randutv_ab(ConstMatrixView(m, n, lda, a), cfg, workers);
+        put(t, r.t);
+        if (u) put(u, r.u);
+        if (v) put(v, r.v);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception(), residual);
     }
 }
 

@@ -149,3 +149,18 @@ def test_generators_equal_reference():
     assert np.array_equal(oracle.geometric_matrix(60, 60, 0.9, 3),
                           oracle.geometric_matrix(60, 60, 0.9, 3, impl="ref"))
     assert np.array_equal(oracle.normal_stream(5, 12345, 500), oracle.normal_stream(5, 12345, 500, impl="ref"))
+
+
+@pytest.mark.skipif(not oracle.available("ref"), reason="reference library not built")
+def test_reference_ab_driver_for_cpu_baseline():
+    # bench.py's CPU baseline also times the reference's multi-threaded algorithm-by-blocks
+    # driver (randutv_ab.hpp:46): same contract as randutv(), bitwise identical for any
+    # worker count, b | n required.
+    a = oracle.geometric_matrix(64, 64, 0.9, 3, impl="ref")
+    t1, u1, v1 = oracle.ref_randutv_ab(a, b=16, q=1, seed=2, workers=1)
+    t4, u4, v4 = oracle.ref_randutv_ab(a, b=16, q=1, seed=2, workers=4)
+    assert np.array_equal(t1, t4) and np.array_equal(u1, u4) and np.array_equal(v1, v4)
+    assert np.linalg.norm(a - u1 @ t1 @ v1.T) / np.linalg.norm(a) < 1e-13
+    assert np.all(np.tril(t1, -1) == 0.0)
+    with pytest.raises(oracle.OracleError):
+        oracle.ref_randutv_ab(oracle.gaussian_matrix(60, 60, 1), b=16, q=1, seed=2, workers=2)
