@@ -147,9 +147,9 @@ def reference_sample(n=1000, b=B_DEF, q=Q_DEF):
     return oracle.flops(n, b, q) / dt / 1e9, dt
 
 
-def reference_ab_sample(n=1024, b=B_DEF, q=Q_DEF, workers=None):
+def reference_ab_sample(n=2048, b=B_DEF, q=Q_DEF, workers=None):
     """The reference's multi-threaded algorithm-by-blocks driver (randutv_ab, every host
-    thread) on the same family; it needs b | n, hence n = 1024 (8 x 128)."""
+    thread) on the same family; it needs b | n, hence n = 2048 (16 x 128)."""
     import oracle
     workers = workers or os.cpu_count() or 1
     a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A, impl="ref")
@@ -164,11 +164,11 @@ def best_reference():
     (value GFLOP/s, seconds, cores, sample text)."""
     v1, dt1 = reference_sample(1000)
     try:
-        v2, dt2, w = reference_ab_sample(1024)
+        v2, dt2, w = reference_ab_sample(2048)
     except Exception:  # the AB driver is an extra; the blocked one always exists
         v2, dt2, w = -1.0, 0.0, 1
     if v2 > v1:
-        return v2, dt2, w, (f"reference randutv_ab (algorithm-by-blocks, {w} threads) on n=1024 of the config-2 "
+        return v2, dt2, w, (f"reference randutv_ab (algorithm-by-blocks, {w} threads) on n=2048 of the config-2 "
                             f"family (b=128, q=2, geometric), {dt2:.2f} s; single-thread blocked randutv() on "
                             f"n=1000: {v1:.2f} GFLOP/s")
     return v1, dt1, 1, (f"reference randutv() (blocked, single thread by contract) on n=1000 of the config-2 "
