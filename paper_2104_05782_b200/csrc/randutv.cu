@@ -142,12 +142,15 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
     // kernels leave ~130 SMs idle).  Stream A first waits for the caller's
     // stream (the input may still be in flight there); the call ends with a
     // host synchronisation on A, so the results are complete on return.
-    cudaStream_t st = st_in, sB = st_in, sC = st_in;
+    // Stream D (high priority) forms Twy and M = W Twy' of each panel while A
+    // already runs the big W-only product of the apply (X W, resp. W' B).
+    cudaStream_t st = st_in, sB = st_in, sC = st_in, sD = st_in;
     if (overlap) {
         int prio_lo = 0, prio_hi = 0;
         RUTV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         RUTV_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio_hi));
         RUTV_CUDA(cudaStreamCreateWithPriority(&sC, cudaStreamNonBlocking, prio_hi));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sD, cudaStreamNonBlocking, prio_hi));
         RUTV_CUDA(cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, prio_lo));
         cudaEvent_t e_in;
         RUTV_CUDA(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
@@ -161,7 +164,7 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         ~StreamGuard() {
             if (own) cudaStreamDestroy(s);
         }
-    } sguardA{st, overlap}, sguard{sB, overlap}, sguardC{sC, overlap};
+    } sguardA{st, overlap}, sguard{sB, overlap}, sguardC{sC, overlap}, sguardD{sD, overlap};
     if (prof_overlap) {  // re-anchor the timeline on the critical stream
         prof.st = st;
         prof.mark(P_START);
@@ -204,7 +207,7 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
     double* Yb[2] = {Y.p, Y2.p};
     const char* hoist_env = std::getenv("RUTV_HOIST");
     const bool hoist = !(hoist_env && std::strcmp(hoist_env, "0") == 0);
-    DevBuf ZlA(sb, st), Twy(bb * bb, st), Gram(bb * bb, st), tau(bb + 1, st);
+    DevBuf ZlA(sb, st), Twy(bb * bb, st), Gram(bb * bb, st), tau(bb + 1, st), tauU(bb + 1, st);
     // double-buffered A -> B hand-off
     DevBuf Wv0(sb, st), Wv1(sb, st), Mv0(sb, st), Mv1(sb, st);
     DevBuf Wu0(sb, st), Wu1(sb, st), Mu0(sb, st), Mu1(sb, st);
@@ -226,7 +229,7 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         std::max<int64_t>({gemm_work_elems(n, bb, n), gemm_work_elems(bb, n, n), gemm_work_elems(vr + n, bb, n),
                            gemm_work_elems(bb, bb, n), gemm_work_elems(bb, n, bb), gemm_work_elems(vr + n, bb, bb),
                            1});
-    DevBuf GWA(gw_elems, st), GWB(gw_elems, st), GWC(gw_elems, st);
+    DevBuf GWA(gw_elems, st), GWB(gw_elems, st), GWC(gw_elems, st), GWD(gw_elems, st);
     const int64_t hqw = hqr_work_elems(n, bb);
     DevBuf HQ(hqw, st);
     // allocations are stream-ordered on st; streams B and C must see them
@@ -234,34 +237,39 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         const cudaEvent_t ev = record(st);
         wait(sB, ev);
         wait(sC, ev);
+        wait(sD, ev);
     }
     // declared after every buffer -> destroyed first: stream B drains before any
     // buffer is released (also on the exception path)
     struct JoinGuard {
-        cudaStream_t a, s, c;
+        cudaStream_t a, s, c, d;
         bool own;
         ~JoinGuard() {
             if (own) {
                 cudaStreamSynchronize(a);
                 cudaStreamSynchronize(s);
                 cudaStreamSynchronize(c);
+                cudaStreamSynchronize(d);
             }
         }
-    } jguard{st, sB, sC, overlap};
+    } jguard{st, sB, sC, sD, overlap};
 
     auto gemmA = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
                      const DView& c) { gemm(st, alpha, ta, a, tb, bm, beta, c, GWA.p, gw_elems); };
     auto gemmB = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
                      const DView& c) { gemm(sB, alpha, ta, a, tb, bm, beta, c, GWB.p, gw_elems); };
 
-    // Compact-WY pieces of a packed panel qr (s x p) on stream A: W, Twy, M = W Twy'.
-    auto form_wy = [&](const DView& qr, int64_t p, double* wbuf, double* mbuf) {
+    // Compact-WY pieces of a packed panel qr (s x p): W on stream A, then
+    // Twy (Gram + form_wy_t) and M = W Twy' on stream D; returns D's event.
+    auto form_wy = [&](const DView& qr, int64_t p, const double* taus, double* wbuf, double* mbuf) {
         const int64_t s = qr.rows;
         DView W(s, p, s, wbuf), M(s, p, s, mbuf);
         make_w(st, qr, p, W);
-        gemmA(1.0, Op::T, W, Op::N, W, 0.0, DView(p, p, p, Gram.p));
-        form_t(st, Gram.p, p, tau.p, p, Twy.p, p);
-        gemmA(1.0, Op::N, W, Op::T, DView(p, p, p, Twy.p), 0.0, M);
+        wait(sD, record(st));
+        gemm(sD, 1.0, Op::T, W, Op::N, W, 0.0, DView(p, p, p, Gram.p), GWD.p, gw_elems);
+        form_t(sD, Gram.p, p, taus, p, Twy.p, p);
+        gemm(sD, 1.0, Op::N, W, Op::T, DView(p, p, p, Twy.p), 0.0, M, GWD.p, gw_elems);
+        return record(sD);
     };
 
     uint64_t pos = 0;  // stream position P_i
@@ -297,18 +305,20 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         // ---- V-side QR (:52-53)
         hqr_panel(st, Yv, tau.p, nullptr, 0, HQ.p, hqw);
         prof.mark(P_QRV);
-        form_wy(Yv, b, Wv[par], Mv[par]);
-        const cudaEvent_t evV = record(st);
+        const cudaEvent_t evTv = form_wy(Yv, b, tau.p, Wv[par], Mv[par]);
         prof.mark(P_WYV);
         DView WvV(s, b, s, Wv[par]), MvV(s, b, s, Mv[par]);
-        cudaEvent_t evR = nullptr;
+        cudaEvent_t evR = nullptr, evV = nullptr;
         {  // V-apply, critical rows: T22 (:140).  Panel-first look-ahead: the
            // U-side QR only needs T22 Q_v's first b columns, so those are
            // updated first on stream A and the other s-b columns on stream C,
-           // overlapping the panel QR.
+           // overlapping the panel QR.  Zx = X W needs only W: it runs while
+           // stream D forms Twy and M.
             DView X = vt.block(vr + r0, r0, s, s);
             DView Zx(s, b, s, ZxA.p);
             gemmA(1.0, Op::N, X, Op::N, WvV, 0.0, Zx);
+            wait(st, evTv);
+            evV = record(st);  // W_v, M_v ready for stream B
             gemmA(-1.0, Op::N, Zx, Op::T, DView(b, b, s, Mv[par]), 1.0, X.block(0, 0, s, b));
             wait(sC, record(st));
             gemm(sC, -1.0, Op::N, Zx, Op::T, DView(s - b, b, s, Mv[par] + b), 1.0, X.block(0, b, s, s - b),
@@ -331,17 +341,18 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         prof.mark(P_APPLYV);
         // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
         DView panel = t22.block(0, 0, s, b);
-        hqr_panel(st, panel, tau.p, nullptr, 0, HQ.p, hqw);
+        hqr_panel(st, panel, tauU.p, nullptr, 0, HQ.p, hqw);
         prof.mark(P_QRU);
-        form_wy(panel, b, Wu[par], Mu[par]);
+        const cudaEvent_t evTu = form_wy(panel, b, tauU.p, Wu[par], Mu[par]);
         copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
         prof.mark(P_WYU);
         DView WuV(s, b, s, Wu[par]), MuV(s, b, s, Mu[par]);
         wait(st, evR);
-        {  // Q_u' on T22(:, b:) (:147)
+        {  // Q_u' on T22(:, b:) (:147); Zl = W_u' B overlaps D's Twy / M_u
             DView B = t22.block(0, b, s, s - b);
             DView Zl(b, s - b, b, ZlA.p);
             gemmA(1.0, Op::T, WuV, Op::N, B, 0.0, Zl);
+            wait(st, evTu);
             gemmA(-1.0, Op::N, MuV, Op::N, Zl, 1.0, B);
             if (hoist_next) {  // Y' = P - Zl^T (M_u(b:, :)^T G')
                 const int64_t s2 = s - b;

@@ -47,21 +47,21 @@ __global__ void __launch_bounds__(512, 1) __cluster_dims__(1, 1, 1) k(int mode, 
             const int par = j & 1;
             double vals[16];
             if (mode & 16) {  // shuffles only
-                const double wkl = x[lane & 15] * 1e-9;
+                const double wkl = (x[0] + lane) * 1e-9;
                 double sacc = 0.0;
 #pragma unroll
                 for (int kk = 1; kk < 16; ++kk) sacc += __shfl_sync(0xffffffffu, wkl, kk);
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) vals[kk] = x[kk] + sacc;
             } else if (mode & 32) {  // FMAs only (w_k from a register)
-                const double wk0 = x[lane & 15] * 1e-9;
+                const double wk0 = (x[0] + lane) * 1e-9;
 #pragma unroll
                 for (int kk = 1; kk < 16; ++kk) x[kk] -= (wk0 + kk) * x[0];
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) vals[kk] = x[1] * x[kk];
             } else if (mode & 64) {  // w_k through shared memory (broadcast LDS.128)
                 __shared__ __align__(16) double wks[16][16];
-                if (lane < 16) wks[warp][lane] = x[lane & 15] * 1e-9;
+                if (lane < 16) wks[warp][lane] = (x[0] + lane) * 1e-9;
                 __syncwarp();
 #pragma unroll
                 for (int k2 = 0; k2 < 8; ++k2) {
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(512, 1) __cluster_dims__(1, 1, 1) k(int mode, 
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) vals[kk] = x[1] * x[kk];
             } else if (mode & 4) {
-                const double wkl = x[lane & 15] * 1e-9;
+                const double wkl = (x[0] + lane) * 1e-9;
 #pragma unroll
                 for (int kk = 1; kk < 16; ++kk) { const double wk = __shfl_sync(0xffffffffu, wkl, kk); x[kk] -= wk * x[0]; }
 #pragma unroll
