@@ -149,7 +149,10 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         int prio_lo = 0, prio_hi = 0;
         RUTV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         RUTV_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio_hi));
-        RUTV_CUDA(cudaStreamCreateWithPriority(&sC, cudaStreamNonBlocking, prio_hi));
+        // C (look-ahead GEMMs that run beside the panel QR) one level below A:
+        // a pending QR cluster must not wait behind C's CTAs for its 16 SMs.
+        const int prio_mid = prio_hi < prio_lo ? prio_hi + 1 : prio_hi;
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sC, cudaStreamNonBlocking, prio_mid));
         RUTV_CUDA(cudaStreamCreateWithPriority(&sD, cudaStreamNonBlocking, prio_hi));
         RUTV_CUDA(cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, prio_lo));
         cudaEvent_t e_in;
@@ -308,7 +311,7 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         const cudaEvent_t evTv = form_wy(Yv, b, tau.p, Wv[par], Mv[par]);
         prof.mark(P_WYV);
         DView WvV(s, b, s, Wv[par]), MvV(s, b, s, Mv[par]);
-        cudaEvent_t evR = nullptr, evV = nullptr;
+        cudaEvent_t evR = nullptr, evV = nullptr, evPan = nullptr;
         {  // V-apply, critical rows: T22 (:140).  Panel-first look-ahead: the
            // U-side QR only needs T22 Q_v's first b columns, so those are
            // updated first on stream A and the other s-b columns on stream C,
@@ -320,7 +323,18 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
             wait(st, evTv);
             evV = record(st);  // W_v, M_v ready for stream B
             gemmA(-1.0, Op::N, Zx, Op::T, DView(b, b, s, Mv[par]), 1.0, X.block(0, 0, s, b));
-            wait(sC, record(st));
+            evPan = record(st);  // panel columns updated: C may start (enqueued after QR_u)
+        }
+        prof.mark(P_APPLYV);
+        // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
+        DView panel = t22.block(0, 0, s, b);
+        hqr_panel(st, panel, tauU.p, nullptr, 0, HQ.p, hqw);
+        prof.mark(P_QRU);
+        {  // stream C, enqueued after the QR_u launch so the QR cluster gets its SMs
+           // before C's CTAs fill the GPU: the other s-b columns of the V-apply
+            DView X = vt.block(vr + r0, r0, s, s);
+            DView Zx(s, b, s, ZxA.p);
+            wait(sC, evPan);
             gemm(sC, -1.0, Op::N, Zx, Op::T, DView(s - b, b, s, Mv[par] + b), 1.0, X.block(0, b, s, s - b),
                  GWC.p, gw_elems);
             // Sketch hoisting.  The next trailing matrix is T22' = B(b:, :) - M_u(b:, :) Zl
@@ -338,11 +352,6 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
             }
             evR = record(sC);
         }
-        prof.mark(P_APPLYV);
-        // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
-        DView panel = t22.block(0, 0, s, b);
-        hqr_panel(st, panel, tauU.p, nullptr, 0, HQ.p, hqw);
-        prof.mark(P_QRU);
         const cudaEvent_t evTu = form_wy(panel, b, tauU.p, Wu[par], Mu[par]);
         copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
         prof.mark(P_WYU);
