@@ -82,7 +82,26 @@ __global__ void __launch_bounds__(512, 1) __cluster_dims__(1, 1, 1) k(int mode, 
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) vals[kk] = x[kk];
             }
-            if (mode & 8) {
+            if (mode & 128) {  // transposed shared-memory reduction instead of the butterfly
+                __shared__ double tr[8][32 * 17];
+                double* tw = tr[warp];
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) tw[lane * 17 + kk] = vals[kk];
+                __syncwarp();
+                const int col = lane & 15, h = lane >> 4;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                for (int r = 0; r < 16; r += 4) {
+                    a0 += tw[(h * 16 + r) * 17 + col];
+                    a1 += tw[(h * 16 + r + 1) * 17 + col];
+                    a2 += tw[(h * 16 + r + 2) * 17 + col];
+                    a3 += tw[(h * 16 + r + 3) * 17 + col];
+                }
+                double v = (a0 + a1) + (a2 + a3);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                vals[0] = v;
+                __syncwarp();
+            } else if (mode & 8) {
 #pragma unroll
                 for (int lvl = 0; lvl < 4; ++lvl) {
                     const int o = 16 >> lvl, n = 8 >> lvl; const bool up = (lane & o) != 0;
@@ -120,7 +139,7 @@ __global__ void __launch_bounds__(512, 1) __cluster_dims__(1, 1, 1) k(int mode, 
 
 int main() {
     double* o; long long* c; cudaMalloc(&o, 1024 * 8); cudaMalloc(&c, 8);
-    for (int mode : {0, 4, 16, 32, 64, 8, 1, 3, 12, 13, 15, 64 + 8 + 3}) {
+    for (int mode : {0, 8, 128, 64 + 8 + 3, 64 + 128 + 3, 4 + 8 + 3, 4 + 128 + 3}) {
         long long h = 0;
         for (int rep = 0; rep < 3; ++rep) {
             k<<<1, 512>>>(mode, o, c);
