@@ -2,9 +2,10 @@
 //
 // The reference factors every panel with column-by-column Householder
 // (proj/src/householder.cpp:48-67), whose 128 dependent column steps make the
-// panel QR latency-bound on the GPU (qr_reg.cu: ~2 us per column).  For a
-// full-rank s x w panel Y (w <= 128, s >= 2w) the same factorization is
-// obtained from level-3 work plus three small w x w factorizations:
+// panel QR latency-bound on the GPU (qr_reg.cu: ~2 us per column, 250-360 us
+// per 128-column panel).  For a full-rank s x w panel Y (16 <= w <= 128,
+// s >= 2w) the same factorization is obtained from level-3 work plus small
+// w x w factorizations:
 //
 //   Cholesky-QR2:  R1 = chol(Y'Y), Q1 = Y R1^{-1};  R2 = chol(Q1'Q1),
 //                  Q = Q1 R2^{-1};  R = R2 R1      (R_jj > 0)
@@ -18,14 +19,28 @@
 // The packed result (R above the diagonal, V below) and tau are exactly what
 // the Householder kernel produces, up to rounding.
 //
-// Status: opt-in (RUTV_CHOLQR=1), see enabled() below.
-// Safety: the path is taken only when it is numerically sound; otherwise the
-// panel is left untouched and the caller runs the Householder kernel:
-//   * Cholesky breakdown (pivot <= 0 or not finite) in either pass, or
-//     min/max diag(R1) < 1e-7 (Cholesky-QR2 needs cond(Y) well below 1/sqrt(eps));
-//   * an LU pivot |tau_j| < 0.25 (a reflector close to the identity: the
+// The small factorizations (Cholesky + triangular inverse, LU + inverse) run
+// in ONE CTA each, blocked by 32: a 32 x 32 diagonal block is factored (and
+// inverted) by one warp in registers with shuffles only, every off-diagonal
+// block product is a 32 x 32 warp tile of DMMA (mma.sync m16n8k4 f64) from
+// shared memory -- a handful of CTA barriers per 32 columns instead of two
+// per column.
+//
+// Safety: the result is only valid when the path is numerically sound; each
+// panel ORs a flag word on the device:
+//   * 1/4: Cholesky breakdown (pivot <= 0 or not finite) in pass 1 / pass 2;
+//   * 2: min/max diag(R1) < 1e-7 (Cholesky-QR2 needs cond(Y) well below 1/sqrt(eps));
+//   * 16: Q1'Q1 farther than 0.1 from I (pass 1 lost too much orthogonality);
+//   * 8: an LU pivot |tau_j| < 0.25 (a reflector close to the identity: the
 //     reconstruction divides by tau_j).
-// A flag word is read back on the host (one stream synchronisation per panel).
+// Two modes:
+//   * deferred (the factorization driver, RUTV_CHOLQR=2): the packed result is
+//     written in place without any host synchronisation and the flag word is
+//     shared by the whole factorization; the driver reads it once at the end
+//     and, if any panel was unsafe, re-runs the factorization with the
+//     Householder kernels (randutv.cu);
+//   * immediate (RUTV_CHOLQR=1, other callers): the flag is read back after the
+//     panel and the caller falls back to the Householder kernel on failure.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -37,348 +52,471 @@
 
 namespace rutv {
 
-constexpr int kCT = 512;
+namespace {
 
-// Register-blocked factorizations of a p x p block (p <= 128) by one CTA of
-// 512 threads: thread (tx, ty) = (tid & 31, tid >> 5) owns rows ty + 16 a
-// (a < 8) and columns tx + 32 b (b < 4) -- 32 entries in registers; a row
-// belongs to one warp, so the pivot-row work is warp-uniform.  A step
-// publishes the pivot row / column in shared memory (double-buffered) and
-// every thread updates its own entries: two barriers per step, no
-// shared-memory traffic for the matrix itself.
+constexpr int kST = 256;  // threads of the small-factorization kernels (8 warps)
+constexpr int kW = kST / 32;
+constexpr unsigned kFull = 0xffffffffu;
 
-// X = R^{-1} for the upper triangular R held in shared memory Rs (column-major,
-// leading dimension LD): back substitution from the last row, X in registers.
-__device__ __forceinline__ void upper_inverse(const double* Rs, int LD, int p, double (&x)[8][4], double* xrow2,
-                                              int tx, int ty) {
+// phase clocks of the last small-factorization launches (debug, rutv_b200_debug_cqr_clocks)
+__device__ long long g_cqr_clk[128];
+#define CQR_CLK(slot) \
+    if (threadIdx.x == 0) g_cqr_clk[(slot)] = clock64()
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};\n"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a0), "d"(a1), "d"(b));
+}
+
+// Warp tile: acc (32 x 32) += A (32 x 32) B (32 x 32) with element accessors
+// fa(i, k), fb(k, j).  Lane (g, t) = (lane >> 2, lane & 3); accumulator
+// acc[mt][nt][r] is element (16 mt + g + 8 (r >= 2), 8 nt + 2 t + (r & 1)).
+template <class FA, class FB>
+__device__ __forceinline__ void mma32(double (&acc)[2][4][4], FA fa, FB fb) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int k = 0; k < 32; k += 4) {
+        double a[2][2], b[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) x[a][b] = (ty + 16 * a == tx + 32 * b) ? 1.0 : 0.0;
-    for (int i = p - 1; i >= 0; --i) {
-        double* xrow = xrow2 + (i & 1) * 128;
-        const double rinv = 1.0 / Rs[i + i * LD];
-        if (ty == (i & 15)) {  // row i owned by warp i % 16
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int k = tx + 32 * b;
-                    const bool hit = (ty + 16 * a == i) && k >= i && k < p;
-                    const double v = x[a][b] * rinv;
-                    x[a][b] = hit ? v : x[a][b];
-                    if (hit) xrow[k] = v;
-                }
+        for (int mt = 0; mt < 2; ++mt) {
+            a[mt][0] = fa(16 * mt + g, k + t);
+            a[mt][1] = fa(16 * mt + g + 8, k + t);
         }
-        __syncthreads();
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int r = ty + 16 * a;
-            if (r < i) {
-                const double rri = Rs[r + i * LD];
+        for (int nt = 0; nt < 4; ++nt) b[nt] = fb(k + t, 8 * nt + g);
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int k = tx + 32 * b;
-                    if (k >= i && k < p) x[a][b] -= rri * xrow[k];
-                }
-            }
-        }
-        __syncthreads();
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
     }
 }
 
-// Upper Cholesky G = R'R, then R^{-1}.  flag |= 1 (breakdown), 2 (diag ratio < 1e-7).
-__global__ void __launch_bounds__(kCT) chol_inv_kernel(const double* __restrict__ g, int64_t ldg, int p, double* r,
-                                                       double* rinv, int* flag, int check_ratio) {
-    extern __shared__ double Rs[];  // p x LD
-    __shared__ double rowb[2][128];
-    __shared__ double dpub[2];
-    const int LD = p + 1, tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-    double a[8][4];
+__device__ __forceinline__ void zero32(double (&acc)[2][4][4]) {
 #pragma unroll
-    for (int ai = 0; ai < 8; ++ai)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-            const int i = ty + 16 * ai, k = tx + 32 * bi;
-            a[ai][bi] = (i < p && k < p) ? g[i + static_cast<int64_t>(k) * ldg] : 0.0;
-        }
-    if (tid == 0) dpub[0] = a[0][0];
-    __syncthreads();
-    bool bad = false;
-    for (int j = 0; j < p; ++j) {
-        const int par = j & 1;
-        const double d = dpub[par];
-        if (!(d > 0.0) || !isfinite(d)) bad = true;
-        const double rj = bad ? 1.0 : sqrt(d), inv = 1.0 / rj;
-        // row j of R (branch-free over the owned entries: a computed index
-        // would move the register array to local memory)
-        if (ty == (j & 15)) {  // row j owned by warp j % 16
+        for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-                for (int bi = 0; bi < 4; ++bi) {
-                    const int i = ty + 16 * ai, k = tx + 32 * bi;
-                    const bool hit = (i == j) && k >= j && k < p;
-                    const double v = k == j ? rj : a[ai][bi] * inv;
-                    a[ai][bi] = hit ? v : a[ai][bi];
-                    if (hit) rowb[par][k] = v;
-                }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int ai = 0; ai < 8; ++ai) {
-            const int i = ty + 16 * ai;
-            if (i > j && i < p) {
-                const double ri = rowb[par][i];
-#pragma unroll
-                for (int bi = 0; bi < 4; ++bi) {
-                    const int k = tx + 32 * bi;
-                    if (k >= i && k < p) a[ai][bi] -= ri * rowb[par][k];
-                }
-            }
-        }
-        if (ty == ((j + 1) & 15) && tx == ((j + 1) & 31)) {
-#pragma unroll
-            for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-                for (int bi = 0; bi < 4; ++bi)
-                    if (ty + 16 * ai == j + 1 && tx + 32 * bi == j + 1) dpub[par ^ 1] = a[ai][bi];
-        }
-        __syncthreads();
-    }
-    // R (upper) to global and shared memory
-#pragma unroll
-    for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-            const int i = ty + 16 * ai, k = tx + 32 * bi;
-            if (i < p && k < p) {
-                const double v = i <= k ? a[ai][bi] : 0.0;
-                r[i + static_cast<int64_t>(k) * p] = v;
-                Rs[i + k * LD] = v;
-            }
-        }
-    __syncthreads();
-    if (tid == 0) {
-        double mn = INFINITY, mx = 0.0;
-        for (int j = 0; j < p; ++j) {
-            mn = fmin(mn, Rs[j + j * LD]);
-            mx = fmax(mx, Rs[j + j * LD]);
-        }
-        if (bad) atomicOr(flag, check_ratio ? 1 : 4);
-        if (check_ratio && !(mn > 1e-7 * mx)) atomicOr(flag, 2);
-    }
-    double x[8][4];
-    upper_inverse(Rs, LD, p, x, &rowb[0][0], tx, ty);
-#pragma unroll
-    for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-            const int i = ty + 16 * ai, k = tx + 32 * bi;
-            if (i < p && k < p) rinv[i + static_cast<int64_t>(k) * p] = i <= k ? x[ai][bi] : 0.0;
-        }
+            for (int r = 0; r < 4; ++r) acc[mt][nt][r] = 0.0;
 }
 
-// LU without pivoting of B = I - Q(0:p, 0:p): L1 strictly lower, U upper,
-// tau = diag(U), then U^{-1}.  |pivot| < 0.25 sets flag bit 8.
-__global__ void __launch_bounds__(kCT) lu_inv_kernel(const double* __restrict__ q, int64_t ldq, int p, double* l1,
-                                                     double* u, double* uinv, double* tau, int* flag) {
-    extern __shared__ double Us[];  // p x LD
-    __shared__ double rowb[2][128], colb[2][128];
-    __shared__ double dpub[2];
-    const int LD = p + 1, tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-    double a[8][4];
+// visit every accumulator element: f(i, j, value)
+template <class F>
+__device__ __forceinline__ void each32(const double (&acc)[2][4][4], F f) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int ai = 0; ai < 8; ++ai)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-            const int i = ty + 16 * ai, k = tx + 32 * bi;
-            a[ai][bi] = (i < p && k < p) ? (i == k ? 1.0 : 0.0) - q[i + static_cast<int64_t>(k) * ldq] : 0.0;
-        }
-    if (tid == 0) dpub[0] = a[0][0];
-    __syncthreads();
-    bool bad = false;
-    for (int j = 0; j < p; ++j) {
-        const int par = j & 1;
-        const double piv = dpub[par];
-        if (!(fabs(piv) >= 0.25) || !isfinite(piv)) bad = true;
-        const double inv = 1.0 / (bad ? 1.0 : piv);
-        // column j: multipliers below the diagonal; row j of U (branch-free)
-        if (tx == (j & 31) || ty == (j & 15)) {
+        for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-                for (int bi = 0; bi < 4; ++bi) {
-                    const int i = ty + 16 * ai, k = tx + 32 * bi;
-                    const bool colhit = (k == j) && i > j && i < p;
-                    const double m = a[ai][bi] * inv;
-                    a[ai][bi] = colhit ? m : a[ai][bi];
-                    if (colhit) colb[par][i] = m;
-                    if ((i == j) && k > j && k < p) rowb[par][k] = a[ai][bi];
-                }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int ai = 0; ai < 8; ++ai) {
-            const int i = ty + 16 * ai;
-            if (i > j && i < p) {
-                const double li = colb[par][i];
-#pragma unroll
-                for (int bi = 0; bi < 4; ++bi) {
-                    const int k = tx + 32 * bi;
-                    if (k > j && k < p) a[ai][bi] -= li * rowb[par][k];
-                }
-            }
-        }
-        if (ty == ((j + 1) & 15) && tx == ((j + 1) & 31)) {
-#pragma unroll
-            for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-                for (int bi = 0; bi < 4; ++bi)
-                    if (ty + 16 * ai == j + 1 && tx + 32 * bi == j + 1) dpub[par ^ 1] = a[ai][bi];
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-            const int i = ty + 16 * ai, k = tx + 32 * bi;
-            if (i < p && k < p) {
-                l1[i + static_cast<int64_t>(k) * p] = i > k ? a[ai][bi] : 0.0;
-                const double uv = i <= k ? a[ai][bi] : 0.0;
-                u[i + static_cast<int64_t>(k) * p] = uv;
-                Us[i + k * LD] = uv;
-                if (i == k) tau[i] = uv;
-            }
-        }
-    __syncthreads();
-    if (tid == 0 && bad) atomicOr(flag, 8);
-    double x[8][4];
-    upper_inverse(Us, LD, p, x, &rowb[0][0], tx, ty);
-#pragma unroll
-    for (int ai = 0; ai < 8; ++ai)
-#pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-            const int i = ty + 16 * ai, k = tx + 32 * bi;
-            if (i < p && k < p) uinv[i + static_cast<int64_t>(k) * p] = i <= k ? x[ai][bi] : 0.0;
-        }
+            for (int r = 0; r < 4; ++r) f(16 * mt + g + (r >= 2 ? 8 : 0), 8 * nt + 2 * t + (r & 1), acc[mt][nt][r]);
 }
 
-// Blocked (32-wide) right-looking Cholesky G = R'R of a p x p block (p <= 128)
-// in shared memory: per block step the 32 x 32 diagonal block is factored by
-// one warp (__syncwarp only), the block row by forward substitution (one
-// column per thread, the 32 unknowns in registers) and the trailing block by
-// a rank-32 update -- 3 CTA barriers per 32 columns instead of 2 per column.
-__global__ void __launch_bounds__(kCT) chol_blocked_kernel(const double* __restrict__ g, int64_t ldg, int p,
-                                                           double* r, int64_t ldr, int* flag, int check_ratio) {
-    extern __shared__ double A[];
-    const int NB = (p + 31) >> 5, P = NB * 32, LD = P + 1;
+// Shared-memory matrix: column-major P x P, LD = P + 4 (LD = 4 mod 16: the
+// DMMA fragment loads of a half-warp hit 16 distinct bank pairs).
+struct SMat {
+    double* a;
+    int ld;
+    __device__ __forceinline__ double& operator()(int i, int k) const { return a[i + k * ld]; }
+};
+
+// Column-oriented back substitution in one warp: lane k gets column k of
+// X = U^{-1} for the 32 x 32 upper block at (j0, j0) of M with reciprocal
+// diagonal dinv[j0..]; x[m] for m <= k (0 above).
+__device__ __forceinline__ void warp_upper_inv(const SMat& M, int j0, const double* dinv, double (&x)[32]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+        const double xi = x[i] * dinv[j0 + i];
+        x[i] = xi;
+#pragma unroll
+        for (int m = 0; m < i; ++m) x[m] -= M(j0 + m, j0 + i) * xi;
+    }
+}
+
+__host__ __device__ inline size_t small_smem_bytes(int p) {
+    const int P = (p + 31) / 32 * 32;
+    // A (P x (P+4)), dinv, dg, rowb (2 x 32), XD, XL, tmp (3 x 32 x 36)
+    return (static_cast<size_t>(P) * (P + 4) + 2 * P + 64 + 5 * 32 * 36) * sizeof(double);
+}
+
+constexpr int TL = 36;  // leading dimension of the 32 x 32 scratch blocks
+
+// A(i, k) = src(i, k) for i, k < p, identity padding up to P; by columns
+// (warp w: columns w, w + 8, ...; lanes: rows), 16 loads in flight per thread.
+template <class F>
+__device__ __forceinline__ void load_square(const SMat& A, int p, int P, F src) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+    for (int k0 = warp; k0 < P; k0 += 4 * kW) {
+        double t[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int k = k0 + u * kW, i = lane + 32 * r;
+                t[u][r] = (i < p && k < p) ? src(i, k) : (i == k ? 1.0 : 0.0);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int k = k0 + u * kW, i = lane + 32 * r;
+                if (i < P && k < P) A(i, k) = t[u][r];
+            }
+    }
+}
+
+// f(i, k) for i in [r0, r1), k in [c0, c1), by columns (coalesced global stores)
+template <class F>
+__device__ __forceinline__ void for_rect(int r0, int r1, int c0, int c1, F f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = c0 + warp; k < c1; k += kW)
+        for (int i = r0 + lane; i < r1; i += 32) f(i, k);
+}
+
+// X = U^{-1} of the upper factor is built one block column per step:
+//   X_IJ = -(sum_{L=I..J-1} X_IL U_LJ) X_JJ,   I < J,
+// X(i, k), i < k, stored TRANSPOSED in A's strictly lower part (A(k, i)),
+// X(k, k) = dinv[k].  Part 1 (with the block-row phase): T_I = sum X_IL U_LJ.
+__device__ __forceinline__ double xinv(const SMat& A, const double* dinv, int i, int k) {
+    const double v = A(k, i);
+    return i < k ? v : (i == k ? dinv[i] : 0.0);
+}
+
+__device__ __forceinline__ void inv_part1(const SMat& A, const double* dinv, double* tmp, int J, int task0) {
+    const int warp = threadIdx.x >> 5, j0 = 32 * J;
+    for (int I = 0; I < J; ++I) {
+        if ((task0 + I) % kW != warp) continue;
+        const int i0 = 32 * I;
+        double acc[2][4][4];
+        zero32(acc);
+        mma32(
+            acc, [&](int i, int m) { return xinv(A, dinv, i0 + i, i0 + m); },
+            [&](int m, int c) { return A(i0 + m, j0 + c); });
+        for (int L = I + 1; L < J; ++L) {
+            const int l0 = 32 * L;
+            mma32(
+                acc, [&](int i, int m) { return A(l0 + m, i0 + i); }, [&](int m, int c) { return A(l0 + m, j0 + c); });
+        }
+        double* T = tmp + I * 32 * TL;
+        each32(acc, [&](int i, int j, double v) { T[i + j * TL] = v; });
+    }
+}
+
+// Part 2 (with the trailing phase): X_IJ = -T_I X_JJ (X_JJ in XD, column-major, ld TL)
+__device__ __forceinline__ void inv_part2(const SMat& A, const double* XD, const double* tmp, int J, int task0) {
+    const int warp = threadIdx.x >> 5, j0 = 32 * J;
+    for (int I = 0; I < J; ++I) {
+        if ((task0 + I) % kW != warp) continue;
+        const int i0 = 32 * I;
+        const double* T = tmp + I * 32 * TL;
+        double acc[2][4][4];
+        zero32(acc);
+        mma32(
+            acc, [&](int i, int m) { return T[i + m * TL]; }, [&](int m, int c) { return XD[m + c * TL]; });
+        each32(acc, [&](int i, int j, double v) { A(j0 + j, i0 + i) = -v; });
+    }
+}
+
+// Upper Cholesky G = R'R (p x p, p <= 128), X = R^{-1}; optionally Rp = R R1
+// (pass 2: the final R = R2 R1).  Flags: breakdown -> brk_bit; pass 1
+// (check_ratio): min/max diag(R) < 1e-7 -> 2; pass 2 (check_orth):
+// max |G - I| > 0.1 -> 16.
+__global__ void __launch_bounds__(kST) cqr_chol_kernel(const double* __restrict__ g, int64_t ldg, int p, double* r,
+                                                       double* rinv, const double* __restrict__ r1, double* rp,
+                                                       int* flag, int brk_bit, int check_ratio, int check_orth) {
+    extern __shared__ double sm[];
+    const int NB = (p + 31) >> 5, P = NB * 32;
+    const SMat A{sm, P + 4};
+    double* dinv = sm + static_cast<size_t>(P) * (P + 4);
+    double* rowb = dinv + 2 * P;  // [2][32]
+    double* XD = rowb + 64;       // X_JJ
+    double* tmp = XD + 2 * 32 * TL;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int e = tid; e < P * P; e += kCT) {
-        const int i = e % P, k = e / P;
-        A[i + k * LD] = (i < p && k < p) ? g[i + static_cast<int64_t>(k) * ldg] : (i == k ? 1.0 : 0.0);
-    }
+    const int base = r1 ? 16 : 0;
+    CQR_CLK(base);
+    load_square(A, p, P, [&](int i, int k) { return g[i + static_cast<int64_t>(k) * ldg]; });
     __syncthreads();
+    if (check_orth) {
+        bool bad_orth = false;
+        for_rect(0, p, 0, p, [&](int i, int k) { bad_orth |= fabs(A(i, k) - (i == k ? 1.0 : 0.0)) > 0.1; });
+        if (__any_sync(kFull, bad_orth) && lane == 0) atomicOr(flag, 16);
+    }
+    CQR_CLK(base + 1);
     bool bad = false;
     for (int J = 0; J < NB; ++J) {
         const int j0 = 32 * J;
-        if (warp == 0) {  // diagonal block in registers: lane k holds column j0 + k
+        if (warp == 0) {
+            // diagonal block in registers: lane k holds column j0 + k; row c of
+            // R broadcast through shared memory
             double v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = A[(j0 + i) + (j0 + lane) * LD];
+            for (int i = 0; i < 32; ++i) v[i] = A(j0 + i, j0 + lane);
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
-                const double d = __shfl_sync(0xffffffffu, v[c], c);
+                const double d = __shfl_sync(kFull, v[c], c);
                 if (!(d > 0.0) || !isfinite(d)) bad = true;
-                const double rc = bad ? 1.0 : sqrt(d), inv = 1.0 / rc;
+                const double inv = bad ? 1.0 : rsqrt(d), rc = bad ? 1.0 : d * inv;
                 v[c] = lane == c ? rc : (lane > c ? v[c] * inv : v[c]);  // row c of R
+                double* rb = rowb + (c & 1) * 32;
+                rb[lane] = v[c];
+                if (lane == c) dinv[j0 + c] = inv;
+                __syncwarp();
 #pragma unroll
-                for (int i = c + 1; i < 32; ++i) {
-                    const double rci = __shfl_sync(0xffffffffu, v[c], i);  // R(c, i) from lane i
-                    if (lane >= i) v[i] -= rci * v[c];
+                for (int i = 0; i < 32; ++i) {
+                    if (i > c) {
+                        const double rci = rb[i];  // R(c, i)
+                        if (lane >= i) v[i] -= rci * v[c];
+                    }
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 32; ++i) A[(j0 + i) + (j0 + lane) * LD] = v[i];
-        }
-        __syncthreads();
-        const int k0 = j0 + 32;
-        for (int k = k0 + tid; k < P; k += kCT) {  // block row: R_JJ' X = A(J, k)
+            for (int i = 0; i < 32; ++i)
+                if (i <= lane) A(j0 + i, j0 + lane) = v[i];
+            __syncwarp();
             double x[32];
-            double* ak = A + k * LD + j0;
+            warp_upper_inv(A, j0, dinv, x);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                double acc = ak[c];
-#pragma unroll
-                for (int i = 0; i < c; ++i) acc -= A[(j0 + i) + (j0 + c) * LD] * x[i];
-                x[c] = acc / A[(j0 + c) + (j0 + c) * LD];
-            }
-#pragma unroll
-            for (int c = 0; c < 32; ++c) ak[c] = x[c];
+            for (int m = 0; m < 32; ++m) XD[m + lane * TL] = x[m];
         }
         __syncthreads();
-        const int m = P - k0;
-        if (m > 0) {  // trailing: A(i, k) -= sum_c R(c, i) R(c, k), i <= k; warp -> rows, lanes -> columns
-            for (int ii = warp; ii < m; ii += kCT / 32) {
-                const int i = k0 + ii;
-                const double* ri = A + i * LD + j0;
-                for (int kk = lane; kk < m; kk += 32) {
-                    const int k = k0 + kk;
-                    if (k < i) continue;
-                    const double* rk = A + k * LD + j0;
-                    double acc = 0.0;
-#pragma unroll 8
-                    for (int c = 0; c < 32; ++c) acc += ri[c] * rk[c];
-                    A[i + k * LD] -= acc;
-                }
-            }
+        CQR_CLK(base + 2 + 3 * J);
+        const int nr = NB - 1 - J;
+        // block row R(J, K) = X_JJ' A(J, K), K > J (in place); X part 1
+        for (int K = J + 1 + warp; K < NB; K += kW) {
+            const int k0 = 32 * K;
+            double acc[2][4][4];
+            zero32(acc);
+            mma32(
+                acc, [&](int i, int m) { return XD[m + i * TL]; }, [&](int m, int c) { return A(j0 + m, k0 + c); });
+            __syncwarp();
+            each32(acc, [&](int i, int j, double v) { A(j0 + i, k0 + j) = v; });
         }
+        inv_part1(A, dinv, tmp, J, nr);
         __syncthreads();
+        CQR_CLK(base + 3 + 3 * J);
+        // X_JJ into the diagonal block's lower triangle; trailing
+        // A(K, L) -= R(J, K)' R(J, L), J < K <= L; X part 2
+        for (int e = tid; e < 32 * 32; e += kST) {
+            const int m = e & 31, k = e >> 5;
+            if (m < k) A(j0 + k, j0 + m) = XD[m + k * TL];
+        }
+        int task = 0;
+        for (int K = J + 1; K < NB; ++K)
+            for (int L = K; L < NB; ++L, ++task) {
+                if (task % kW != warp) continue;
+                const int k0 = 32 * K, l0 = 32 * L;
+                double acc[2][4][4];
+                zero32(acc);
+                mma32(
+                    acc, [&](int i, int m) { return A(j0 + m, k0 + i); }, [&](int m, int c) { return A(j0 + m, l0 + c); });
+                each32(acc, [&](int i, int j, double v) { A(k0 + i, l0 + j) -= v; });
+            }
+        inv_part2(A, XD, tmp, J, task);
+        __syncthreads();
+        CQR_CLK(base + 4 + 3 * J);
     }
-    for (int e = tid; e < p * p; e += kCT) {
-        const int i = e % p, k = e / p;
-        r[i + static_cast<int64_t>(k) * ldr] = i <= k ? A[i + k * LD] : 0.0;
-    }
-    if (tid == 0) {
+    if (warp == 0 && __any_sync(kFull, bad) && lane == 0) atomicOr(flag, brk_bit);
+    CQR_CLK(base + 14);
+    for_rect(0, p, 0, p, [&](int i, int k) {
+        r[i + static_cast<int64_t>(k) * p] = i <= k ? A(i, k) : 0.0;
+        rinv[i + static_cast<int64_t>(k) * p] = xinv(A, dinv, i, k);
+    });
+    if (check_ratio && warp == 0) {
         double mn = INFINITY, mx = 0.0;
-        for (int j = 0; j < p; ++j) {
-            mn = fmin(mn, A[j + j * LD]);
-            mx = fmax(mx, A[j + j * LD]);
+        for (int j = lane; j < p; j += 32) {
+            mn = fmin(mn, A(j, j));
+            mx = fmax(mx, A(j, j));
         }
-        if (bad) atomicOr(flag, check_ratio ? 1 : 4);
-        if (check_ratio && !(mn > 1e-7 * mx)) atomicOr(flag, 2);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+        }
+        if (lane == 0 && !(mn > 1e-7 * mx)) atomicOr(flag, 2);
+    }
+    if (r1) {  // Rp = R R1 (both upper): block (I, K) = sum_{L=I..K} R_IL R1_LK, R1 from L2
+        int t2 = 0;
+        for (int I = 0; I < NB; ++I)
+            for (int K = I; K < NB; ++K, ++t2) {
+                if (t2 % kW != warp) continue;
+                const int i0 = 32 * I, k0 = 32 * K;
+                double acc[2][4][4];
+                zero32(acc);
+                for (int L = I; L <= K; ++L) {
+                    const int l0 = 32 * L;
+                    mma32(
+                        acc, [&](int i, int m) { return (l0 + m >= i0 + i) ? A(i0 + i, l0 + m) : 0.0; },
+                        [&](int m, int c) {
+                            const int row = l0 + m, col = k0 + c;
+                            const bool in = row < p && col < p;
+                            const double v = r1[in ? row + static_cast<int64_t>(col) * p : 0];
+                            return row > col ? 0.0 : (in ? v : (row == col ? 1.0 : 0.0));
+                        });
+                }
+                each32(acc, [&](int i, int j, double v) {
+                    const int row = i0 + i, col = k0 + j;
+                    if (row < p && col < p) rp[row + static_cast<int64_t>(col) * p] = row <= col ? v : 0.0;
+                    if (I != K && k0 + i < p && i0 + j < p)  // the strictly lower block (K, I) is zero
+                        rp[(k0 + i) + static_cast<int64_t>(i0 + j) * p] = 0.0;
+                });
+            }
     }
     __syncthreads();
-    if (warp == 0 && bad && lane == 0) atomicOr(flag, check_ratio ? 1 : 4);
+    CQR_CLK(base + 15);
 }
 
-namespace {
+// LU without pivoting of B = I - Q(0:p, 0:p) (p <= 128).  Writes the packed
+// top block [R upper (from rfull); L strictly lower] to top (ld ldtop),
+// tau = diag(U), and U^{-1} (p x p, ld p).  |pivot| < 0.25 -> flag 8.
+__global__ void __launch_bounds__(kST) cqr_lu_kernel(const double* __restrict__ q, int64_t ldq, int p,
+                                                     const double* __restrict__ rfull, double* top, int64_t ldtop,
+                                                     double* uinv, double* tau, int* flag) {
+    extern __shared__ double sm[];
+    const int NB = (p + 31) >> 5, P = NB * 32;
+    const SMat A{sm, P + 4};
+    double* dinv = sm + static_cast<size_t>(P) * (P + 4);
+    double* rowb = dinv + 2 * P;
+    double* XD = rowb + 64;     // U_JJ^{-1}
+    double* XL = XD + 32 * TL;  // L_JJ^{-1}
+    double* tmp = XL + 32 * TL;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int base = 32;
+    CQR_CLK(base);
+    load_square(A, p, P, [&](int i, int k) { return (i == k ? 1.0 : 0.0) - q[i + static_cast<int64_t>(k) * ldq]; });
+    __syncthreads();
+    CQR_CLK(base + 1);
+    bool bad = false;
+    for (int J = 0; J < NB; ++J) {
+        const int j0 = 32 * J;
+        if (warp == 0) {
+            double v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = A(j0 + i, j0 + lane);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const double piv = __shfl_sync(kFull, v[c], c);
+                if (!(fabs(piv) >= 0.25) || !isfinite(piv)) bad = true;
+                const double inv = __drcp_rn(bad ? 1.0 : piv);
+                if (lane == c) dinv[j0 + c] = inv;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if (i > c) {
+                        if (lane == c) v[i] *= inv;  // multiplier L(i, c)
+                        const double li = __shfl_sync(kFull, v[i], c);
+                        if (lane > c) v[i] -= li * v[c];
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) A(j0 + i, j0 + lane) = v[i];
+            __syncwarp();
+            double x[32];
+            warp_upper_inv(A, j0, dinv, x);  // XD = U_JJ^{-1} (lane k: column k)
+#pragma unroll
+            for (int m = 0; m < 32; ++m) XD[m + lane * TL] = x[m];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+#pragma unroll
+                for (int m = i + 1; m < 32; ++m) x[m] -= A(j0 + m, j0 + i) * x[i];
+#pragma unroll
+            for (int m = 0; m < 32; ++m) XL[m + lane * TL] = x[m];
+        }
+        __syncthreads();
+        CQR_CLK(base + 2 + 3 * J);
+        const int nr = NB - 1 - J;
+        // L_JJ out; U(J, K) = XL A(J, K) and L(K, J) = A(K, J) XU for K > J; X part 1
+        for_rect(j0, j0 + 32, j0, j0 + 32, [&](int i, int k) {
+            if (i > k && i < p && k < p) top[i + static_cast<int64_t>(k) * ldtop] = A(i, k);
+        });
+        for (int task = warp; task < 2 * nr; task += kW) {
+            const int K = J + 1 + (task % nr), k0 = 32 * K;
+            double acc[2][4][4];
+            zero32(acc);
+            if (task < nr) {
+                mma32(
+                    acc, [&](int i, int m) { return XL[i + m * TL]; }, [&](int m, int c) { return A(j0 + m, k0 + c); });
+                __syncwarp();
+                each32(acc, [&](int i, int j, double v) { A(j0 + i, k0 + j) = v; });
+            } else {
+                mma32(
+                    acc, [&](int i, int m) { return A(k0 + i, j0 + m); }, [&](int m, int c) { return XD[m + c * TL]; });
+                __syncwarp();
+                each32(acc, [&](int i, int j, double v) { A(k0 + i, j0 + j) = v; });
+            }
+        }
+        inv_part1(A, dinv, tmp, J, 2 * nr);
+        __syncthreads();
+        CQR_CLK(base + 3 + 3 * J);
+        // L(K, J) out; X_JJ into the diagonal block's lower triangle; trailing
+        // A(K, L) -= L(K, J) U(J, L), K, L > J; X part 2
+        for_rect(j0 + 32, P, j0, j0 + 32, [&](int i, int k) {
+            if (i < p && k < p) top[i + static_cast<int64_t>(k) * ldtop] = A(i, k);
+        });
+        for (int e = tid; e < 32 * 32; e += kST) {
+            const int m = e & 31, k = e >> 5;
+            if (m < k) A(j0 + k, j0 + m) = XD[m + k * TL];
+        }
+        for (int task = warp; task < nr * nr; task += kW) {
+            const int K = J + 1 + task / nr, L = J + 1 + task % nr, k0 = 32 * K, l0 = 32 * L;
+            double acc[2][4][4];
+            zero32(acc);
+            mma32(
+                acc, [&](int i, int m) { return A(k0 + i, j0 + m); }, [&](int m, int c) { return A(j0 + m, l0 + c); });
+            each32(acc, [&](int i, int j, double v) { A(k0 + i, l0 + j) -= v; });
+        }
+        inv_part2(A, XD, tmp, J, nr * nr);
+        __syncthreads();
+        CQR_CLK(base + 4 + 3 * J);
+    }
+    if (warp == 0 && __any_sync(kFull, bad) && lane == 0) atomicOr(flag, 8);
+    CQR_CLK(base + 14);
+    for_rect(0, p, 0, p, [&](int i, int k) {
+        if (i <= k) top[i + static_cast<int64_t>(k) * ldtop] = rfull[i + static_cast<int64_t>(k) * p];
+        if (i == k) tau[i] = A(i, i);
+        uinv[i + static_cast<int64_t>(k) * p] = xinv(A, dinv, i, k);
+    });
+    __syncthreads();
+    CQR_CLK(base + 16);
+}
 
-// packed panel: R on and above the diagonal, V1 below it in rows < p, V2 rows >= p
-__global__ void commit_kernel(int64_t s, int p, const double* __restrict__ rr, const double* __restrict__ l1,
-                              const double* __restrict__ l2, int64_t ldl2, double* a, int64_t lda) {
+
+__global__ void commit_kernel(int64_t s, int p, const double* __restrict__ topb, const double* __restrict__ l2,
+                              int64_t ldl2, double* a, int64_t lda) {
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < s * p;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e % s, j = e / s;
-        double v;
-        if (i <= j) v = rr[i + j * p];
-        else if (i < p) v = l1[i + j * p];
-        else v = l2[(i - p) + j * ldl2];
-        a[i + j * lda] = v;
+        a[i + j * lda] = i < p ? topb[i + j * p] : l2[(i - p) + j * ldl2];
     }
 }
 
-// Opt-in (RUTV_CHOLQR=1): correct (tests/test_gpu_cholqr.py) but its three
-// single-CTA w x w factorizations are still latency-bound (~150 us each at
-// w = 128), so the cluster Householder kernel stays the default.
-bool enabled() {
+void small_attr() {
+    static bool done = false;
+    if (done) return;
+    const int bytes = static_cast<int>(small_smem_bytes(128));
+    RUTV_CUDA(cudaFuncSetAttribute(cqr_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    RUTV_CUDA(cudaFuncSetAttribute(cqr_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = true;
+}
+
+// immediate mode (RUTV_CHOLQR=1) for callers outside the factorization driver
+bool immediate_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("RUTV_CHOLQR");
         return e && std::strcmp(e, "1") == 0;
     }();
     return on;
 }
+
+thread_local int* t_deferred_flag = nullptr;
 
 void gemm_w(cudaStream_t st, double alpha, Op ta, const DView& a, Op tb, const DView& b, double beta,
             const DView& c) {
@@ -390,92 +528,119 @@ void gemm_w(cudaStream_t st, double alpha, Op ta, const DView& a, Op tb, const D
 
 }  // namespace
 
+// Deferred mode in the factorization driver: opt-in (RUTV_CHOLQR=2).  The
+// three single-CTA 128-column factorizations are still latency-bound
+// (~70 us Cholesky, ~70 us LU on B200, tools/time_cqr.py), so a panel costs
+// about as much as the cluster Householder kernel (qr_reg.cu) and the
+// Householder path stays the default.
+bool cholqr_deferred_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RUTV_CHOLQR");
+        return e && std::strcmp(e, "2") == 0;
+    }();
+    return on;
+}
+
+void cholqr_set_deferred(int* dflag) { t_deferred_flag = dflag; }
+
 bool qr_panel_fast(cudaStream_t st, const DView& y, double* tau) {
     const int64_t s = y.rows, p = y.cols;
-    if (!enabled() || p < 16 || p > 128 || s < 2 * p) return false;
-    static bool attr = false;
-    if (!attr) {
-        RUTV_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        RUTV_CUDA(cudaFuncSetAttribute(chol_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        RUTV_CUDA(cudaFuncSetAttribute(lu_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
-    }
-    const size_t sm = static_cast<size_t>(p) * (p + 1) * sizeof(double);
-    const int64_t P32 = (p + 31) / 32 * 32;
-    const size_t smb = static_cast<size_t>(P32) * (P32 + 1) * sizeof(double);
+    int* dflag = t_deferred_flag;
+    if (!dflag && !immediate_enabled()) return false;
+    if (p < 16 || p > 128 || s < 2 * p) return false;
+    small_attr();
+    const size_t smb = small_smem_bytes(static_cast<int>(p));
     const int64_t pp = p * p;
-    DevBuf G(pp, st), R1(pp, st), R1i(pp, st), R2(pp, st), R2i(pp, st), R(pp, st), L1(pp, st), U(pp, st),
-        Ui(pp, st), tu(p + 1, st), Q1(s * p, st), Qb(s * p, st), F(1, st);
-    int* flag = reinterpret_cast<int*>(F.p);
-    RUTV_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    DevBuf G(pp, st), R1(pp, st), R1i(pp, st), R2(pp, st), R2i(pp, st), R(pp, st), Ui(pp, st), Q1(s * p, st),
+        Qb(s * p, st);
+    DevBuf F(1, st), Top(dflag ? 1 : pp, st), Tu(dflag ? 1 : p + 1, st);
+    int* flag = dflag;
+    if (!flag) {
+        flag = reinterpret_cast<int*>(F.p);
+        RUTV_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    }
     const DView Gv(p, p, p, G.p), Q1v(s, p, s, Q1.p), Qbv(s, p, s, Qb.p);
+    const int pi = static_cast<int>(p);
     // pass 1
     gemm_w(st, 1.0, Op::T, y, Op::N, y, 0.0, Gv);
-    chol_blocked_kernel<<<1, kCT, smb, st>>>(G.p, p, static_cast<int>(p), R1.p, p, flag, 1);
+    cqr_chol_kernel<<<1, kST, smb, st>>>(G.p, p, pi, R1.p, R1i.p, nullptr, nullptr, flag, 1, 1, 0);
     note_launch();
     RUTV_CHECK_LAUNCH();
-    tri_inv_upper(st, R1.p, p, p, R1i.p, p);
     gemm_w(st, 1.0, Op::N, y, Op::N, DView(p, p, p, R1i.p), 0.0, Q1v);
-    // pass 2
+    // pass 2 (+ R = R2 R1)
     gemm_w(st, 1.0, Op::T, Q1v, Op::N, Q1v, 0.0, Gv);
-    chol_blocked_kernel<<<1, kCT, smb, st>>>(G.p, p, static_cast<int>(p), R2.p, p, flag, 0);
+    cqr_chol_kernel<<<1, kST, smb, st>>>(G.p, p, pi, R2.p, R2i.p, R1.p, R.p, flag, 4, 0, 1);
     note_launch();
     RUTV_CHECK_LAUNCH();
-    tri_inv_upper(st, R2.p, p, p, R2i.p, p);
     gemm_w(st, 1.0, Op::N, Q1v, Op::N, DView(p, p, p, R2i.p), 0.0, Qbv);
-    gemm_w(st, 1.0, Op::N, DView(p, p, p, R2.p), Op::N, DView(p, p, p, R1.p), 0.0, DView(p, p, p, R.p));
-    // reconstruction
-    lu_inv_kernel<<<1, kCT, sm, st>>>(Qb.p, s, static_cast<int>(p), L1.p, U.p, Ui.p, tu.p, flag);
+    // reconstruction: top block and tau, then V2 = -Q(p:s, :) U^{-1}
+    double* topp = dflag ? y.data : Top.p;
+    const int64_t ldtop = dflag ? y.ld : p;
+    double* taup = dflag ? tau : Tu.p;
+    cqr_lu_kernel<<<1, kST, smb, st>>>(Qb.p, s, pi, R.p, topp, ldtop, Ui.p, taup, flag);
     note_launch();
     RUTV_CHECK_LAUNCH();
-    // V2 = -Q(p:s, :) U^{-1}, into Q1 (rows 0..s-p)
+    if (dflag) {
+        gemm_w(st, -1.0, Op::N, Qbv.block(p, 0, s - p, p), Op::N, DView(p, p, p, Ui.p), 0.0,
+               y.block(p, 0, s - p, p));
+        return true;
+    }
     gemm_w(st, -1.0, Op::N, Qbv.block(p, 0, s - p, p), Op::N, DView(p, p, p, Ui.p), 0.0, DView(s - p, p, s, Q1.p));
     int hflag = 1;
     RUTV_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     RUTV_CUDA(cudaStreamSynchronize(st));
-    static const bool force = std::getenv("RUTV_CHOLQR_FORCE") != nullptr;  // debug: commit regardless
-    if (force) {
-        std::fprintf(stderr, "[rutv] cholqr forced commit, flag was %d\n", hflag);
-        hflag = 0;
-    }
     if (hflag != 0) {
         static const bool dbg = std::getenv("RUTV_DEBUG") != nullptr;
-        if (dbg) std::fprintf(stderr, "[rutv] cholqr fallback s=%lld w=%lld flag=%d\n", static_cast<long long>(s),
-                              static_cast<long long>(p), hflag);
+        if (dbg)
+            std::fprintf(stderr, "[rutv] cholqr fallback s=%lld w=%lld flag=%d\n", static_cast<long long>(s),
+                         static_cast<long long>(p), hflag);
         return false;
     }
     commit_kernel<<<static_cast<unsigned>(std::min<int64_t>((s * p + 255) / 256, 4 * kNumSMs)), 256, 0, st>>>(
-        s, static_cast<int>(p), R.p, L1.p, Q1.p, s, y.data, y.ld);
+        s, pi, Top.p, Q1.p, s, y.data, y.ld);
     note_launch();
     RUTV_CHECK_LAUNCH();
-    RUTV_CUDA(cudaMemcpyAsync(tau, tu.p, static_cast<size_t>(p) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    RUTV_CUDA(cudaMemcpyAsync(tau, Tu.p, static_cast<size_t>(p) * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return true;
 }
 
 }  // namespace rutv
 
 // Test hooks (not part of the public header): the small factorizations alone.
+// rutv_b200_debug_chol: G (p x p, ld p) -> R, R^{-1}; returns the flag word.
 extern "C" int rutv_b200_debug_chol(const double* g, int p, double* r, double* rinv) {
+    rutv::small_attr();
     int* flag = nullptr;
     cudaMalloc(&flag, sizeof(int));
     cudaMemset(flag, 0, sizeof(int));
-    cudaFuncSetAttribute(rutv::chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    rutv::chol_inv_kernel<<<1, rutv::kCT, static_cast<size_t>(p) * (p + 1) * 8>>>(g, p, p, r, rinv, flag, 1);
+    rutv::cqr_chol_kernel<<<1, rutv::kST, rutv::small_smem_bytes(p)>>>(g, p, p, r, rinv, nullptr, nullptr, flag, 1, 1,
+                                                                       0);
     int h = -1;
     cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost);
     cudaFree(flag);
     return h;
 }
 
+// rutv_b200_debug_lu: Q (ldq) -> L1 (strictly lower of the packed top with a
+// zero R), U = T V1', U^{-1}, tau; returns the flag word.
 extern "C" int rutv_b200_debug_lu(const double* q, int64_t ldq, int p, double* l1, double* u, double* uinv,
                                   double* tau) {
+    rutv::small_attr();
     int* flag = nullptr;
+    double* zr = nullptr;
     cudaMalloc(&flag, sizeof(int));
+    cudaMalloc(&zr, sizeof(double) * p * p);
     cudaMemset(flag, 0, sizeof(int));
-    cudaFuncSetAttribute(rutv::lu_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    rutv::lu_inv_kernel<<<1, rutv::kCT, static_cast<size_t>(p) * (p + 1) * 8>>>(q, ldq, p, l1, u, uinv, tau, flag);
+    cudaMemset(zr, 0, sizeof(double) * p * p);
+    rutv::cqr_lu_kernel<<<1, rutv::kST, rutv::small_smem_bytes(p)>>>(q, ldq, p, zr, l1, p, uinv, tau, flag);
+    (void)u;
     int h = -1;
     cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(zr);
     cudaFree(flag);
     return h;
+}
+
+extern "C" int rutv_b200_debug_cqr_clocks(long long* out64) {
+    return cudaMemcpyFromSymbol(out64, rutv::g_cqr_clk, sizeof(long long) * 128) == cudaSuccess ? 0 : 1;
 }

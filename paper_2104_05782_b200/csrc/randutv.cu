@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -100,7 +101,10 @@ const char* kPhaseNames[P_N] = {"start", "sketch", "qr_v", "apply_v", "qr_u", "a
 
 }  // namespace
 
-void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArgs& fa) {
+// One factorization.  With `cqr` the panel QRs take the Cholesky-QR2 path in
+// deferred mode (cholqr.cu); returns false -- before anything is written to
+// the caller's outputs -- when one of its panels was numerically unsafe.
+static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const FactorArgs& fa, bool cqr) {
     const int64_t b = fa.b;
     configure_pool(device);
     Profiler prof;
@@ -235,6 +239,13 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
     DevBuf GWA(gw_elems, st), GWB(gw_elems, st), GWC(gw_elems, st), GWD(gw_elems, st);
     const int64_t hqw = hqr_work_elems(n, bb);
     DevBuf HQ(hqw, st);
+    DevBuf Cqf(1, st);  // Cholesky-QR2 safety flags of every panel (deferred mode)
+    int* cqr_flag = cqr ? reinterpret_cast<int*>(Cqf.p) : nullptr;
+    if (cqr_flag) RUTV_CUDA(cudaMemsetAsync(cqr_flag, 0, sizeof(int), st));
+    struct DeferGuard {
+        explicit DeferGuard(int* f) { cholqr_set_deferred(f); }
+        ~DeferGuard() { cholqr_set_deferred(nullptr); }
+    } dguard(cqr_flag);
     // allocations are stream-ordered on st; streams B and C must see them
     {
         const cudaEvent_t ev = record(st);
@@ -503,6 +514,16 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         prof.mark(P_BETA);
     }
 
+    if (cqr_flag) {  // any unsafe Cholesky-QR2 panel: the caller re-runs with Householder
+        int hflag = 0;
+        RUTV_CUDA(cudaMemcpyAsync(&hflag, cqr_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        RUTV_CUDA(cudaStreamSynchronize(st));
+        if (hflag != 0) {
+            static const bool dbg = std::getenv("RUTV_DEBUG") != nullptr;
+            if (dbg) std::fprintf(stderr, "[rutv] cholqr flag %d: re-running with Householder panels\n", hflag);
+            return false;
+        }
+    }
     // results out (T rows vr.., V rows 0..n)
     copy_view(st, DView(n, n, fa.ldt, fa.dT), tmat);
     if (bu && fa.dU) copy_view(st, DView(n, n, fa.ldu, fa.dU), umat);
@@ -523,6 +544,12 @@ void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArg
         if (hs[static_cast<size_t>(4 * k)] == RUTV_ERR_CONVERGENCE)
             throw Error(RUTV_ERR_CONVERGENCE, "jacobi sweeps exhausted after 30 sweeps",
                         hs[static_cast<size_t>(4 * k + 1)]);
+    return true;
+}
+
+void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArgs& fa) {
+    if (cholqr_deferred_enabled() && factorize_impl(st_in, device, n, fa, true)) return;
+    factorize_impl(st_in, device, n, fa, false);
 }
 
 int last_profile(const char** names, double* ms, int cap) {

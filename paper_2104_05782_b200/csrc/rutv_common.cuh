@@ -138,6 +138,10 @@ void tri_inv_upper(cudaStream_t stream, const double* r, int64_t ldr, int64_t p,
 // Panel QR through Cholesky-QR2 + Householder reconstruction (cholqr.cu); false
 // (panel untouched) when the fast path is not applicable or not safe.
 bool qr_panel_fast(cudaStream_t stream, const DView& a, double* tau);
+// Deferred mode of the fast path (the factorization driver): panels commit
+// without a host check and OR their safety flags into *dflag (null: off).
+void cholqr_set_deferred(int* dflag);
+bool cholqr_deferred_enabled();
 
 // One-sided Jacobi SVD of a square block (jacobi_svd.cpp:39-148).  Writes U, sigma, V
 // (n x n, ld n).  Status (code, residual, kept, sweeps) is written to

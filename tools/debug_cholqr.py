@@ -21,7 +21,12 @@ for s, p in ((2000, 128), (700, 100), (300, 37)):
     T = torch.zeros(p, dtype=torch.float64, device="cuda")
     fl = L.rutv_b200_debug_lu(P(Qd), s, p, P(L1), P(U), P(Ui), P(T))
     _, tau_ref, _ = oracle.hqr(Y)
-    print("   lu flag", fl, "tau err", np.max(np.abs(T.cpu().numpy() - tau_ref)), "Uinv err", np.max(np.abs(to_np(Ui) @ to_np(U) - np.eye(p))))
+    Lh = np.tril(to_np(L1), -1) + np.eye(p)
+    Uh = Lh @ np.zeros((p, p))
+    Bm = np.eye(p) - Q[:p]
+    Ue = np.linalg.solve(Lh, Bm)
+    print("   lu flag", fl, "tau err", np.max(np.abs(T.cpu().numpy() - tau_ref)), "Uinv err", np.max(np.abs(to_np(Ui) @ Ue - np.eye(p))),
+          "LU err", np.max(np.abs(np.tril(Ue, -1))))
     # full panel QR through the C ABI
     A = cm_cuda(Y); tau = torch.zeros(p, dtype=torch.float64, device="cuda")
     L.rutv_b200_set_stream(C.c_uint64(torch.cuda.current_stream().cuda_stream))
