@@ -579,9 +579,16 @@ JCfg choose(int n, int count = 1) {
     }
     // Each round streams the CTA's rows of B and V through shared memory, so
     // time per round scales with the rows per CTA: spread a problem over more
-    // CTAs while the whole batch still fits in one wave of SMs.
-    while (c.vsm && c.cs * 2 <= g_jmax_cluster && static_cast<int64_t>(count) * c.cs * 2 <= kNumSMs &&
-           (n + 2 * c.cs - 1) / (2 * c.cs) >= 16 && !use_rs(n, c.cs * 2)) {
+    // CTAs while the whole batch still fits in one wave of SMs -- down to 32
+    // rows per CTA; below that the per-round DSMEM exchange dominates (B200,
+    // n = 128 batches: 4 CTAs 3.2 ms, 8 CTAs 4.3 ms, 1-2 CTAs 4.7 ms).
+    static const int cs_cap = [] {  // tuning knob: RUTV_JACOBI_CSMAX=k caps the widening at k CTAs
+        const char* e = std::getenv("RUTV_JACOBI_CSMAX");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? v : 1 << 30;
+    }();
+    while (c.vsm && c.cs * 2 <= std::min(g_jmax_cluster, cs_cap) && static_cast<int64_t>(count) * c.cs * 2 <= kNumSMs &&
+           (n + 2 * c.cs - 1) / (2 * c.cs) >= 32 && !use_rs(n, c.cs * 2)) {
         const int cs = c.cs * 2, R = (n + cs - 1) / cs;
         c = {cs, R, 1, 0, jsmem_bytes(n, R, cs, true)};
     }
