@@ -258,24 +258,35 @@ __global__ void __launch_bounds__(kST) cqr_chol_kernel(const double* __restrict_
             double v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = A(j0 + i, j0 + lane);
+            // The chain is kept free of data-dependent control flow: a breakdown
+            // (pivot <= 0 or not finite) only sets the flag -- the panel is then
+            // discarded by the caller -- and 1/R(c, c) is stored after the loop.
+            // The next pivot is formed by its owner lane from its own R(c, c+1)
+            // (no shared-memory round trip on the column chain), with the same
+            // fma as the broadcast update, so the bits agree.
+            double myinv = 1.0;
+            bool brk = false;
+            double d = __shfl_sync(kFull, v[0], 0);
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
-                const double d = __shfl_sync(kFull, v[c], c);
-                if (!(d > 0.0) || !isfinite(d)) bad = true;
-                const double inv = bad ? 1.0 : rsqrt(d), rc = bad ? 1.0 : d * inv;
+                brk |= !(d > 0.0) || !isfinite(d);
+                const double inv = rsqrt(d), rc = d * inv;
                 v[c] = lane == c ? rc : (lane > c ? v[c] * inv : v[c]);  // row c of R
+                myinv = lane == c ? inv : myinv;
+                if (c + 1 < 32) d = __shfl_sync(kFull, __fma_rn(-v[c], v[c], v[c + 1 < 32 ? c + 1 : c]), c + 1);
                 double* rb = rowb + (c & 1) * 32;
                 rb[lane] = v[c];
-                if (lane == c) dinv[j0 + c] = inv;
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     if (i > c) {
                         const double rci = rb[i];  // R(c, i)
-                        if (lane >= i) v[i] -= rci * v[c];
+                        if (lane >= i) v[i] = __fma_rn(-rci, v[c], v[i]);
                     }
                 }
             }
+            dinv[j0 + lane] = myinv;
+            bad |= brk;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
                 if (i <= lane) A(j0 + i, j0 + lane) = v[i];
@@ -399,21 +410,36 @@ __global__ void __launch_bounds__(kST) cqr_lu_kernel(const double* __restrict__ 
             double v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = A(j0 + i, j0 + lane);
+            // Branch-free chain (a small pivot only sets the flag); the next
+            // pivot's multiplier and update go first, the rest of the column's
+            // broadcasts after it.
+            double myinv = 1.0;
+            bool brk = false;
+            double piv = __shfl_sync(kFull, v[0], 0);
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
-                const double piv = __shfl_sync(kFull, v[c], c);
-                if (!(fabs(piv) >= 0.25) || !isfinite(piv)) bad = true;
-                const double inv = __drcp_rn(bad ? 1.0 : piv);
-                if (lane == c) dinv[j0 + c] = inv;
+                brk |= !(fabs(piv) >= 0.25) || !isfinite(piv);
+                const double inv = __drcp_rn(piv);
+                myinv = lane == c ? inv : myinv;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i > c && lane == c) v[i] *= inv;  // multipliers L(i, c)
+                if (c + 1 < 32) {
+                    const int n1 = c + 1 < 32 ? c + 1 : c;
+                    const double l1 = __shfl_sync(kFull, v[n1], c);
+                    if (lane > c) v[n1] = __fma_rn(-l1, v[c], v[n1]);
+                    piv = __shfl_sync(kFull, v[n1], n1);
+                }
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    if (i > c) {
-                        if (lane == c) v[i] *= inv;  // multiplier L(i, c)
+                    if (i > c + 1) {
                         const double li = __shfl_sync(kFull, v[i], c);
-                        if (lane > c) v[i] -= li * v[c];
+                        if (lane > c) v[i] = __fma_rn(-li, v[c], v[i]);
                     }
                 }
             }
+            dinv[j0 + lane] = myinv;
+            bad |= brk;
 #pragma unroll
             for (int i = 0; i < 32; ++i) A(j0 + i, j0 + lane) = v[i];
             __syncwarp();
@@ -530,9 +556,9 @@ void gemm_w(cudaStream_t st, double alpha, Op ta, const DView& a, Op tb, const D
 
 // Deferred mode in the factorization driver: opt-in (RUTV_CHOLQR=2).  The
 // three single-CTA 128-column factorizations are still latency-bound
-// (~70 us Cholesky, ~70 us LU on B200, tools/time_cqr.py), so a panel costs
-// about as much as the cluster Householder kernel (qr_reg.cu) and the
-// Householder path stays the default.
+// (~65 us Cholesky, ~62 us LU on B200, tools/time_cqr.py): a panel costs
+// ~318 us, about the cluster Householder kernel's 250-360 us (qr_reg.cu), so
+// the Householder path stays the default.
 bool cholqr_deferred_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("RUTV_CHOLQR");

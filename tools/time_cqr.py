@@ -19,4 +19,5 @@ c = list(clk)
 out = {}
 for name, b in (("chol1", 0), ("chol2", 16), ("lu", 32)):
     out[name] = [c[b + i] - c[b] if c[b + i] else None for i in range(17)]
+out['chol1_diag0'] = [c[60 + i] - c[1] for i in range(4)]
 print(json.dumps(out))
