@@ -8,6 +8,9 @@
 //                   W'W it needs comes from the DMMA GEMM)
 #include <algorithm>
 
+#include <cstdlib>
+#include <string>
+
 #include "rutv_common.cuh"
 
 namespace rutv {
@@ -322,6 +325,14 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
             double* t, int64_t ldt) {
     if (p == 0) return;
     if (p > 1024) throw Error(RUTV_ERR_NOTIMPL, "form_t: block size above 1024");
+    static const bool rd_only = [] {  // RUTV_FORMT=rd: recursive doubling for every p <= 256 (A/B knob)
+        const char* e = std::getenv("RUTV_FORMT");
+        return e && std::string(e) == "rd";
+    }();
+    if (p <= 128 && !rd_only) {
+        form_t_small(stream, gram, ldg, tau, p, t, ldt);
+        return;
+    }
     if (p <= 256) {
         static int rcap = 0;
         if (!rcap) {

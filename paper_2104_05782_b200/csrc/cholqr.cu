@@ -515,6 +515,79 @@ __global__ void __launch_bounds__(kST) cqr_lu_kernel(const double* __restrict__ 
 }
 
 
+// Compact-WY T factor (householder.cpp:76-97) by inversion: the forward
+// recurrence T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j) is exactly the inverse
+// of the upper triangular U = diag(1/tau) + striu(G), G = W'W, so for
+// p <= 128 with every tau != 0 T = U^{-1} is built by the same blocked
+// inversion as R^{-1} above (diagonal blocks by one warp each, off-diagonal
+// block columns by DMMA) -- one CTA, a few barriers.  A tau = 0 reflector
+// (householder.cpp:26-27: H = I) has no inverse form; that rare panel takes
+// the recurrence column by column.
+__global__ void __launch_bounds__(kST) form_t_inv_kernel(const double* __restrict__ g, int64_t ldg,
+                                                         const double* __restrict__ tau, int p, double* t,
+                                                         int64_t ldt) {
+    extern __shared__ double sm[];
+    const int NB = (p + 31) >> 5, P = NB * 32;
+    const SMat A{sm, P + 4};
+    double* dinv = sm + static_cast<size_t>(P) * (P + 4);  // 1 / U_ii = tau_i
+    double* tmp = dinv + 2 * P + 64 + 2 * 32 * TL;  // the chol kernel's tmp
+    __shared__ int s_zero;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_zero = 0;
+    __syncthreads();
+    load_square(A, p, P, [&](int i, int k) { return g[i + static_cast<int64_t>(k) * ldg]; });
+    for (int i = tid; i < P; i += kST) {
+        const double ti = i < p ? tau[i] : 1.0;
+        dinv[i] = ti;
+        if (ti == 0.0) s_zero = 1;
+    }
+    __syncthreads();
+    if (s_zero) {  // recurrence, column by column (T read back from global)
+        for (int j = 0; j < p; ++j) {
+            const double tj = tau[j];
+            for (int i = tid; i < p; i += kST) {
+                double v;
+                if (i < j) {
+                    double acc = 0.0;
+                    for (int m = i; m < j; ++m) acc += t[i + static_cast<int64_t>(m) * ldt] * A(m, j);
+                    v = -tj * acc;
+                } else {
+                    v = i == j ? tj : 0.0;
+                }
+                t[i + static_cast<int64_t>(j) * ldt] = v;
+            }
+            __syncthreads();
+        }
+        return;
+    }
+    for (int J = warp; J < NB; J += kW) {
+        const int j0 = 32 * J;
+        double x[32];
+        warp_upper_inv(A, j0, dinv, x);
+#pragma unroll
+        for (int m = 0; m < 32; ++m)
+            if (m < lane) A(j0 + lane, j0 + m) = x[m];
+    }
+    __syncthreads();
+    for (int J = 1; J < NB; ++J) {
+        inv_part1(A, dinv, tmp, J, 0);
+        __syncthreads();
+        const int j0 = 32 * J;
+        for (int I = warp; I < J; I += kW) {  // X_IJ = -T_I X_JJ
+            const int i0 = 32 * I;
+            const double* T = tmp + I * 32 * TL;
+            double acc[2][4][4];
+            zero32(acc);
+            mma32(
+                acc, [&](int i, int m) { return T[i + m * TL]; },
+                [&](int m, int c) { return xinv(A, dinv, j0 + m, j0 + c); });
+            each32(acc, [&](int i, int j, double v) { A(j0 + j, i0 + i) = -v; });
+        }
+        __syncthreads();
+    }
+    for_rect(0, p, 0, p, [&](int i, int k) { t[i + static_cast<int64_t>(k) * ldt] = xinv(A, dinv, i, k); });
+}
+
 __global__ void commit_kernel(int64_t s, int p, const double* __restrict__ topb, const double* __restrict__ l2,
                               int64_t ldl2, double* a, int64_t lda) {
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < s * p;
@@ -628,6 +701,21 @@ bool qr_panel_fast(cudaStream_t st, const DView& y, double* tau) {
     RUTV_CHECK_LAUNCH();
     RUTV_CUDA(cudaMemcpyAsync(tau, Tu.p, static_cast<size_t>(p) * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return true;
+}
+
+// T of compact WY for p <= 128 (form_t dispatches here).
+void form_t_small(cudaStream_t stream, const double* gram, int64_t ldg, const double* tau, int64_t p, double* t,
+                  int64_t ldt) {
+    static bool attr = false;
+    if (!attr) {
+        RUTV_CUDA(cudaFuncSetAttribute(form_t_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(small_smem_bytes(128))));
+        attr = true;
+    }
+    form_t_inv_kernel<<<1, kST, small_smem_bytes(static_cast<int>(p)), stream>>>(gram, ldg, tau, static_cast<int>(p),
+                                                                                   t, ldt);
+    note_launch();
+    RUTV_CHECK_LAUNCH();
 }
 
 }  // namespace rutv
