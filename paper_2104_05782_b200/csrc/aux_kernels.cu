@@ -366,23 +366,5 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
     RUTV_CHECK_LAUNCH();
 }
 
-void tri_inv_upper(cudaStream_t stream, const double* r, int64_t ldr, int64_t p, double* x, int64_t ldx) {
-    if (p == 0) return;
-    if (p > 256) throw Error(RUTV_ERR_NOTIMPL, "tri_inv_upper: order above 256");
-    static int rcap = 0;
-    if (!rcap) {
-        rcap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_rd_kernel));
-        RUTV_CUDA(cudaFuncSetAttribute(form_t_rd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rcap));
-    }
-    int64_t xe = 1;
-    for (int64_t h = 16; h < p; h *= 2) xe = std::max(xe, (p + 2 * h - 1) / (2 * h) * h * h);
-    const size_t xs = static_cast<size_t>(xe) * sizeof(double);
-    const size_t msz = static_cast<size_t>(p) * (p + 1) * sizeof(double);
-    const bool in_smem = msz + xs <= static_cast<size_t>(rcap);
-    form_t_rd_kernel<<<1, kFtThreads, in_smem ? msz + xs : xs, stream>>>(r, ldr, nullptr, static_cast<int>(p), x, ldx,
-                                                                      in_smem ? 1 : 0, 1);
-    note_launch();
-    RUTV_CHECK_LAUNCH();
-}
 
 }  // namespace rutv

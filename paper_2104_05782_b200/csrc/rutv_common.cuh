@@ -136,8 +136,6 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
 // The same for p <= 128 by blocked inversion of diag(1/tau) + striu(G) (cholqr.cu).
 void form_t_small(cudaStream_t stream, const double* gram, int64_t ldg, const double* tau, int64_t p,
                   double* t, int64_t ldt);
-// X = R^{-1} for upper triangular R (p <= 256), recursive doubling.
-void tri_inv_upper(cudaStream_t stream, const double* r, int64_t ldr, int64_t p, double* x, int64_t ldx);
 // Panel QR through Cholesky-QR2 + Householder reconstruction (cholqr.cu); false
 // (panel untouched) when the fast path is not applicable or not safe.
 bool qr_panel_fast(cudaStream_t stream, const DView& a, double* tau);
