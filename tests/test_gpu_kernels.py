@@ -205,3 +205,30 @@ def test_svd_block_geometric_diagonal():
     a = np.diag(0.5 ** np.arange(n))
     _, s, _ = _svd_dev(a)
     assert np.max(np.abs(s - 0.5 ** np.arange(n)) / 0.5 ** np.arange(n)) < 1e-13
+
+
+def test_twy_with_identity_reflectors():
+    """Twy when some tau = 0 (householder.cpp:26-27: H = I): form_t's inverse form
+    does not exist there and the kernel takes the recurrence (householder.cpp:76-97)."""
+    import torch
+    s, p = 300, 40
+    a = oracle.gaussian_matrix(s, p, 17)
+    for j in (0, 1, 2):  # leading columns already upper triangular, positive diagonal -> tau_j = 0
+        a[j + 1:, j] = 0.0
+        a[j, j] = abs(a[j, j]) + 1.0
+    qr_ref, tau_ref, twy_ref = oracle.hqr(a)
+    assert np.sum(tau_ref == 0.0) >= 3
+    A = cm_cuda(a)
+    tau = torch.zeros(p, dtype=torch.float64, device="cuda")
+    twy = cm_empty(p, p)
+    rutv.hqr(A, tau, twy)
+    assert np.max(np.abs(tau.cpu().numpy() - tau_ref)) < 1e-12
+    assert np.max(np.abs(to_np(twy) - twy_ref)) < 1e-10
+    # and a panel with every tau != 0 through the inverse form, against the recurrence
+    b = oracle.gaussian_matrix(500, 100, 18)
+    _, tau_b, twy_b = oracle.hqr(b)
+    B = cm_cuda(b)
+    tb = torch.zeros(100, dtype=torch.float64, device="cuda")
+    tw = cm_empty(100, 100)
+    rutv.hqr(B, tb, tw)
+    assert np.max(np.abs(to_np(tw) - twy_b)) < 1e-10 * max(1.0, np.max(np.abs(twy_b)))
