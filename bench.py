@@ -3,27 +3,44 @@
 
 Metric: randUTV FP64 effective GFLOP/s = F(n, b, q) / time, F the reference's
 algorithmic flop count (U and V built).
-Workload (BASELINE.json configs[1]): n = 4000 geometric A = Q1 diag(sigma) Q2^T,
-sigma_i = 10^(-12 (i-1)/(n-1)), b = 128, q = 2, full U, T, V.  A is built on
-the device with the reference's Haar construction (metrics.cpp:95-110) from a
-fixed seed -- synthetic data, no dataset involved.
+
+Workload (default): BASELINE.json configs[4] -- "config 5", the largest
+single-GPU configuration and the north-star target: n = 50000 iid N(0,1) A
+(gaussian_matrix, metrics.cpp:90-93, generated on the device from seed 1),
+b = 512, q = 2, full U, T, V.  `--config 1..4` selects the other BASELINE
+configs (they are parity-test cases, tests/test_gpu_configs.py).  Synthetic
+data, no dataset involved.
 
 A "step" is one complete factorization of that matrix.
-  value : device-resident (A in HBM, outputs in HBM), CUDA events on the stream
-          the library runs on, max over ranks.
-  e2e   : the C-ABI host call rutv_b200_factorize with pinned host buffers:
-          H2D of A and D2H of T, U, V inside the timed region.
-Every input (A 128 MB, state 384 MB) exceeds the 126 MB L2, so no flush is
-needed between iterations.
+  value : device-resident: A and the outputs in HBM (T and V stacked in one
+          buffer, U separate -- factored in place, 4 n^2 doubles = 80 GB at
+          config 5), CUDA events on the stream the library runs on, max over ranks.
+  e2e   : the reference-facing C-ABI host call rutv_b200_factorize with pinned
+          host buffers: H2D of A and D2H of T, U, V inside the timed region.
+          At n >= 20000 it is timed over min(K, --e2e-steps) steps (default 2):
+          one config-5 call is ~44 s and the driver's arm has 1800 s.
+Every input exceeds the 126 MB L2 (config 5: 20 GB A, 60 GB state), so no flush
+is needed between iterations.
 
---impl reference: the reference's own CPU randUTV (oracle/_ref, compiled from
-/root/reference/proj/src unmodified), single-threaded as the reference is by
-contract, timed on a bounded sample of the same workload
-family: n = 1000, b = 128, q = 2, geometric sigma 1 -> 1e-12.
+roofline: the DMMA GEMM kernel (the dominant kernel, ~90 % of the flops):
+achieved = sum 2MNK / sum of CUDA-event-timed GEMM launches over a profiled
+pass with the streams serialised (each event bracket = one launch); at
+n >= 20000 the pass covers the first --profile-steps steps (the largest
+trailing matrices).  traffic = dram bytes per GEMM launch from the committed
+ncu --set full capture of this config (profiles/gemm_traffic_c<cfg>.json), or
+null when none exists.
 
---gpus N > 1 (torchrun): each rank factors its own matrix (independent
-replicas, weak scaling); the 2D block-cyclic sharded path is not wired into
-this bench yet.
+cpu_baseline and --impl reference: the UNMODIFIED reference (oracle/_ref,
+compiled from /root/reference/proj/src) on the box's host cores, on a bounded
+sample of the same config family (same b, q and matrix kind): the faster of its
+multi-threaded algorithm-by-blocks driver (randutv_ab, every host thread; needs
+b | n) and its single-threaded blocked randutv().  The
+config's wall time is extrapolated as F(n, b, q) / (measured GFLOP/s) and
+labelled so.
+
+--gpus N > 1 (torchrun): the 2D block-cyclic sharded factorization of ONE
+matrix (strong scaling, dist.py over NCCL); --replicas runs one independent
+factorization per GPU instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -39,10 +56,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_DEF, B_DEF, Q_DEF = 4000, 128, 2
 SEED_A, SEED_G = 1, 2
 DMMA_PEAK_TFLOPS = 37.1  # profiles/r01_dmma_peak.jsonl: mma.sync f64 burst, 148 SMs, 1.965 GHz
 METRIC = "randUTV FP64 effective GFLOP/s & time at 1/2/4/8 B200; % of FP64 TC peak"
+DEFAULT_CONFIG = 5
 
 
 def log(*a):
@@ -61,8 +78,14 @@ KIND_TEXT = {"gaussian": "iid N(0,1)", "geometric": "geometric sigma 1->1e-12 (H
              "cliff": "sigma=1 (i<=3000) then 1e-3*0.999^(i-3000) (Haar product)"}
 
 
-def workload_name(n, b, q, kind="geometric", cfg=2):
+def workload_name(n, b, q, kind, cfg):
     return f"config{cfg}: n={n} {KIND_TEXT[kind]}, b={b}, q={q}, full U/T/V"
+
+
+def cliff_sigma(n):
+    import numpy as np
+    i = np.arange(1, n + 1)
+    return np.where(i <= 3000, 1.0, 1e-3 * 0.999 ** (i - 3000.0))
 
 
 def make_matrix(rutv, a, kind, seed):
@@ -73,10 +96,16 @@ def make_matrix(rutv, a, kind, seed):
     elif kind == "geometric":
         rutv.spectrum_matrix_device(a, seed, beta=10 ** (-12 / (n - 1)))
     else:
-        import numpy as np
-        i = np.arange(1, n + 1)
-        sig = np.where(i <= 3000, 1.0, 1e-3 * 0.999 ** (i - 3000.0))
-        rutv.spectrum_matrix_device(a, seed, sigma=sig)
+        rutv.spectrum_matrix_device(a, seed, sigma=cliff_sigma(n))
+
+
+def config_dict(args, parallelism):
+    """The `config` object of BOTH arms (identical, so the driver sees the same workload)."""
+    n, b, q = args.n, args.b, args.q
+    return {"workload": workload_name(n, b, q, args.kind, args.config), "n": n, "b": b, "q": q,
+            "flops_per_step": args.flops, "parallelism": parallelism,
+            "l2": f"inputs (A {8 * n * n / 1e9:.3g} GB + {24 * n * n / 1e9:.3g} GB state) exceed the 126 MB L2; "
+                  "no flush"}
 
 
 # ----------------------------------------------------------------- clocks --
@@ -137,77 +166,116 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference --
-def reference_sample(n=1000, b=B_DEF, q=Q_DEF):
-    """Time the unmodified reference randutv() (oracle/_ref) once on the sample (1 thread)."""
+def sample_matrix(kind, n):
+    """Bounded-sample input of the same family, generated by the C restatement
+    (bit-identical to the reference's generators, tests/test_oracle_pin.py)."""
     import oracle
-    a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A, impl="ref")
-    t0 = time.perf_counter()
-    oracle.randutv(a, b=b, q=q, seed=SEED_G, impl="ref")
-    dt = time.perf_counter() - t0
-    return oracle.flops(n, b, q) / dt / 1e9, dt
+    if kind == "gaussian":
+        return oracle.gaussian_matrix(n, n, SEED_A)
+    if kind == "geometric":
+        return oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A)
+    return oracle.spectrum_matrix(n, n, cliff_sigma(n), SEED_A)
 
 
-def reference_ab_sample(n=2048, b=B_DEF, q=Q_DEF, workers=None):
-    """The reference's multi-threaded algorithm-by-blocks driver (randutv_ab, every host
-    thread) on the same family; it needs b | n, hence n = 2048 (16 x 128)."""
-    import oracle
-    workers = workers or os.cpu_count() or 1
-    a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A, impl="ref")
-    t0 = time.perf_counter()
-    oracle.ref_randutv_ab(a, b=b, q=q, seed=SEED_G, workers=workers)
-    dt = time.perf_counter() - t0
-    return oracle.flops(n, b, q) / dt / 1e9, dt, workers
+def sample_sizes(b):
+    """(n for the blocked driver, n for the AB driver) -- a few seconds of CPU work each:
+    two full steps plus the ragged tail for the blocked driver, b | n for the AB driver."""
+    return max(2 * b, 1000), max(4 * b, 2048)
 
 
-def best_reference():
-    """The faster of the reference's two CPU drivers on the box's host cores:
-    (value GFLOP/s, seconds, cores, sample text)."""
-    v1, dt1 = reference_sample(1000)
-    try:
-        v2, dt2, w = reference_ab_sample(2048)
-    except Exception:  # the AB driver is an extra; the blocked one always exists
-        v2, dt2, w = -1.0, 0.0, 1
-    if v2 > v1:
-        return v2, dt2, w, (f"reference randutv_ab (algorithm-by-blocks, {w} threads) on n=2048 of the config-2 "
-                            f"family (b=128, q=2, geometric), {dt2:.2f} s; single-thread blocked randutv() on "
-                            f"n=1000: {v1:.2f} GFLOP/s")
-    return v1, dt1, 1, (f"reference randutv() (blocked, single thread by contract) on n=1000 of the config-2 "
-                        f"family (b=128, q=2, geometric), {dt1:.2f} s")
+class ReferenceSampler:
+    """Times the UNMODIFIED reference on the sample; picks the faster driver once."""
+
+    def __init__(self, b, q, kind):
+        import oracle
+        self.oracle, self.b, self.q, self.kind = oracle, b, q, kind
+        self.n_blk, self.n_ab = sample_sizes(b)
+        self.a_blk = sample_matrix(kind, self.n_blk)
+        self.a_ab = sample_matrix(kind, self.n_ab)
+        self.workers = os.cpu_count() or 1
+        self.driver = None
+
+    def blocked(self):
+        t0 = time.perf_counter()
+        self.oracle.randutv(self.a_blk, b=self.b, q=self.q, seed=SEED_G, impl="ref")
+        dt = time.perf_counter() - t0
+        return self.oracle.flops(self.n_blk, self.b, self.q) / dt / 1e9, dt
+
+    def ab(self):
+        t0 = time.perf_counter()
+        self.oracle.ref_randutv_ab(self.a_ab, b=self.b, q=self.q, seed=SEED_G, workers=self.workers)
+        dt = time.perf_counter() - t0
+        return self.oracle.flops(self.n_ab, self.b, self.q) / dt / 1e9, dt
+
+    def pick(self):
+        v1, dt1 = self.blocked()
+        try:
+            v2, dt2 = self.ab()
+        except Exception:  # the AB driver is an extra; the blocked one always exists
+            v2, dt2 = -1.0, 0.0
+        self.driver = "ab" if v2 > v1 else "blocked"
+        self.first = (v1, dt1, v2, dt2)
+        return (v2, dt2) if self.driver == "ab" else (v1, dt1)
+
+    def sample(self):
+        return self.ab() if self.driver == "ab" else self.blocked()
+
+    def describe(self, dt):
+        v1, dt1, v2, dt2 = self.first
+        fam = f"b={self.b}, q={self.q}, {KIND_TEXT[self.kind]}"
+        if self.driver == "ab":
+            return (f"reference randutv_ab (algorithm-by-blocks, {self.workers} threads) on n={self.n_ab} of the "
+                    f"config family ({fam}), {dt:.2f} s; single-thread blocked randutv() on n={self.n_blk}: "
+                    f"{v1:.2f} GFLOP/s")
+        return (f"reference randutv() (blocked, single thread by contract) on n={self.n_blk} of the config family "
+                f"({fam}), {dt:.2f} s; randutv_ab on n={self.n_ab}: {v2:.2f} GFLOP/s")
+
+    @property
+    def cores(self):
+        return self.workers if self.driver == "ab" else 1
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path on the box's host cores, on the
+    same config (family sample, extrapolated to the config by the flop model)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
-    if not oracle.available("ref"):
-        kind = "port"
-    else:
-        kind = "reference"
-    vals, times, cores, sample = [], [], 1, ""
-    for i in range(args.warmup + args.steps):
-        if kind == "reference":
-            v, dt, cores, sample = best_reference()
-        else:  # the C restatement (only if the reference library is missing)
-            n = 1000
-            a = oracle.geometric_matrix(n, n, 10 ** (-12 / (n - 1)), SEED_A)
+    kind = "reference" if oracle.available("ref") else "port"
+    vals, times = [], []
+    if kind == "reference":
+        rs = ReferenceSampler(args.b, args.q, args.kind)
+        for i in range(args.warmup + args.steps):
+            v, dt = rs.pick() if i == 0 else rs.sample()
+            if i >= args.warmup:
+                vals.append(v)
+                times.append(dt)
+        cores, sample = rs.cores, rs.describe(statistics.median(times))
+    else:  # the C restatement, only if the reference library is missing
+        n = sample_sizes(args.b)[0]
+        a = sample_matrix(args.kind, n)
+        for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            oracle.randutv(a, b=B_DEF, q=Q_DEF, seed=SEED_G)
+            oracle.randutv(a, b=args.b, q=args.q, seed=SEED_G)
             dt = time.perf_counter() - t0
-            v = oracle.flops(n, B_DEF, Q_DEF) / dt / 1e9
-            sample = f"C restatement of randutv() on n={n}, single thread"
-        if i >= args.warmup:
-            vals.append(v)
-            times.append(dt)
+            if i >= args.warmup:
+                vals.append(oracle.flops(n, args.b, args.q) / dt / 1e9)
+                times.append(dt)
+        cores, sample = os.cpu_count() or 1, f"C restatement of randutv() on n={n}"
     value = statistics.median(vals)
-    sample += "; value = F(n,128,2)/t, median over the timed steps"
+    cfg_s = args.flops / (value * 1e9)
+    sample += (f"; value = F(sample)/t, median over the {args.steps} timed steps; config wall time extrapolated "
+               f"as F(n={args.n},b={args.b},q={args.q}) / value = {cfg_s:.0f} s")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1000 * statistics.median(times), 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.n, args.b, args.q, args.kind, args.config), "b": B_DEF,
-                   "q": Q_DEF, "parallelism": f"cpu-{cores}threads"},
+        "ms_per_step": round(1000 * cfg_s, 1), "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 and not args.replicas else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic ({KIND_TEXT[args.kind]}, seed {SEED_A}; bounded sample of the config)",
+        "config": config_dict(args, parallelism(args, args.gpus)),
+        "extrapolated": {"sample_seconds_median": round(statistics.median(times), 3),
+                         "config_seconds": round(cfg_s, 1), "model": "F(n,b,q) / sample GFLOP/s"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
@@ -217,9 +285,29 @@ def run_reference(args):
     return 0
 
 
+def parallelism(args, world):
+    if world <= 1:
+        return "single"
+    if args.replicas:
+        return f"replicas x{world}"
+    from paper_2104_05782_b200.dist import grid_shape
+    P, Q = grid_shape(world)
+    return f"2d-block-cyclic {P}x{Q}"
+
+
 # ------------------------------------------------------------------- B200 --
 def cm(torch, m, n, dev):
     return torch.empty((n, m), dtype=torch.float64, device=dev).T
+
+
+def traffic_for(cfg):
+    """dram bytes per GEMM launch from this config's committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", f"gemm_traffic_c{cfg}.json")
+    try:
+        d = json.load(open(path))
+        return d.get("bytes_per_launch"), os.path.relpath(path, ROOT)
+    except (OSError, ValueError):
+        return None, None
 
 
 def main():
@@ -228,14 +316,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
-                    help="BASELINE.json config (default 2, the single-GPU headline)")
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default 5, the north-star single-GPU configuration)")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--b", type=int, default=None)
     ap.add_argument("--q", type=int, default=None)
-    ap.add_argument("--sharded", action="store_true",
-                    help="N > 1: ONE matrix on the 2D block-cyclic grid (dist.py, NCCL), strong scaling; "
-                         "default: one independent factorization per GPU (weak scaling)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one independent factorization per GPU (weak scaling) instead of the sharded "
+                         "2D block-cyclic factorization of one matrix")
+    ap.add_argument("--sharded", action="store_true", help="(default for N > 1; kept for compatibility)")
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="timed host-pointer steps (default: K, or 2 when n >= 20000)")
+    ap.add_argument("--profile-steps", type=int, default=None,
+                    help="steps of the serialised GEMM-profile pass (default: all, or 12 when n >= 20000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -245,6 +338,12 @@ def main():
     args.b = cfgd["b"] if args.b is None else args.b
     args.q = cfgd["q"] if args.q is None else args.q
     args.kind = cfgd["kind"]
+    big = args.n >= 20000
+    if args.e2e_steps is None:
+        args.e2e_steps = min(args.steps, 2) if big else args.steps
+    if args.profile_steps is None:
+        args.profile_steps = 12 if big else -1
+    args.flops = flops(args.n, args.b, args.q)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -259,19 +358,22 @@ def main():
     dev = torch.device(f"cuda:{local}")
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n, b, q = args.n, args.b, args.q
-    F = rutv.flops(n, b, q)
-    if args.sharded:
-        return run_sharded(args, torch, dist, rutv, world, rank, local, dev, F)
+        if not args.replicas:
+            return run_sharded(args, torch, dist, rutv, world, rank, local, dev, args.flops)
+    n, b, q, F = args.n, args.b, args.q, args.flops
+    assert abs(F - rutv.flops(n, b, q)) <= 1e-9 * F
 
     a = cm(torch, n, n, dev)
     make_matrix(rutv, a, args.kind, SEED_A + rank)
-    t, u, v = cm(torch, n, n, dev), cm(torch, n, n, dev), cm(torch, n, n, dev)
+    # T and V stacked in one buffer (V rows on top): the library factors in place
+    vt = cm(torch, 2 * n, n, dev)
+    t, v = vt[n:, :], vt[:n, :]
+    u = cm(torch, n, n, dev)
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
 
-    def step():
-        rutv.factorize_device(a, t, u, v, b=b, q=q, seed=SEED_G, stream=sh)
+    def step(max_steps=-1):
+        rutv.factorize_device(a, t, u, v, b=b, q=q, seed=SEED_G, stream=sh, max_steps=max_steps)
 
     for _ in range(args.warmup):
         step()
@@ -298,54 +400,16 @@ def main():
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     value = world * F / (ms_max / 1e3) / 1e9
+    diag0 = torch.diagonal(t)[:8].cpu()
 
-    # ---- e2e through the C ABI with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        import ctypes as C
-        import numpy as np
-        ha = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        ha.copy_(a.T.cpu())  # column-major bytes of A
-        ht = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        hu = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        hv = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        o = rutv.make_opts(b=b, q=q, seed=SEED_G, device=local, stream=sh)
-        st = rutv.Status()
-        L = rutv.lib()
-
-        def e2e_step():
-            L.rutv_b200_factorize(C.byref(o), C.c_void_p(ha.data_ptr()), n, n, n, None, 0,
-                                  C.c_void_p(ht.data_ptr()), n, C.c_void_p(hu.data_ptr()), n,
-                                  C.c_void_p(hv.data_ptr()), n, C.byref(st))
-            rutv._raise(st)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        ems = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(world * F / (float(ems.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
-               "ms_per_step": round(float(ems.item()), 3),
-               "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 3 * 8 * n * n}
-        # sanity: the host result matches the device one (same stream of deviates)
-        assert np.allclose(ht.numpy().T[:4, :4], t.cpu().numpy()[:4, :4])
-
-    # ---- roofline of the dominant kernel (DMMA GEMM), separate profiled pass
-    # Streams serialized (RUTV_OVERLAP=0) so each GEMM's event bracket is its own
-    # launch time, not time shared with concurrent kernels of the other streams.
+    # ---- roofline of the dominant kernel (DMMA GEMM), separate profiled pass.
+    # Streams serialised (RUTV_OVERLAP=0) so each GEMM's event bracket is its own
+    # launch; bounded to the first profile_steps steps at large n.
     os.environ["RUTV_GEMM_PROFILE"] = "1"
     os.environ["RUTV_OVERLAP"] = "0"
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    step()
+    step(args.profile_steps)
     p1.record(stream)
     torch.cuda.synchronize()
     pass_ms = p0.elapsed_time(p1)
@@ -353,32 +417,73 @@ def main():
     os.environ["RUTV_OVERLAP"] = "1"
     gp = rutv.gemm_profile()
     gemm_tflops = gp["flops"] / (gp["ms"] / 1e3) / 1e12 if gp["ms"] > 0 else None
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
+    traffic, tsrc = traffic_for(args.config) if (n, b, q) == tuple(CONFIGS[args.config][k] for k in "nbq") \
+        else (None, None)
     roofline = {"bound": "tensor", "achieved": round(gemm_tflops, 3) if gemm_tflops else None,
                 "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(gemm_tflops / DMMA_PEAK_TFLOPS, 4) if gemm_tflops else None,
-                "traffic": traffic, "kernel": "dgemm_kernel (+split-K reduce)",
-                "gemm_ms_per_step": round(gp["ms"], 3), "gemm_launches": gp["launches"],
-                "gemm_share_of_serialized_step": round(gp["ms"] / pass_ms, 4) if pass_ms > 0 else None,
-                "serialized_step_ms": round(pass_ms, 3),
-                "step_frac_of_peak": round(F / (ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS, 4),
+                "traffic": traffic, "traffic_source": tsrc, "kernel": "dgemm_kernel (+split-K reduce)",
+                "gemm_ms_profiled": round(gp["ms"], 3), "gemm_launches_profiled": gp["launches"],
+                "profiled_steps": args.profile_steps if args.profile_steps >= 0 else "all",
+                "gemm_share_of_serialized_pass": round(gp["ms"] / pass_ms, 4) if pass_ms > 0 else None,
+                "serialized_pass_ms": round(pass_ms, 3),
+                "step_frac_of_peak": round(F / (ms_max / 1e3) / 1e12 / DMMA_PEAK_TFLOPS, 4),
                 "peak_source": "measured DMMA burst (profiles/r01_dmma_peak.jsonl); "
                                "MEASURED_PEAKS.json has no FP64 entry"}
+
+    # ---- e2e through the C ABI with pinned host buffers (the device tensors are
+    # released first: the host-pointer call allocates its own 3 n^2 device state)
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        import numpy as np
+        ha = rutv.PinnedMatrix(n, n)
+        torch.from_numpy(ha.array).copy_(a)  # column-major bytes of A, D2H straight into pinned memory
+        del a, vt, t, v, u
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        hout = [rutv.PinnedMatrix(n, n) for _ in range(3)]
+        o = rutv.make_opts(b=b, q=q, seed=SEED_G, device=local, stream=sh)
+        st = rutv.Status()
+        L = rutv.lib()
+
+        def e2e_step():
+            L.rutv_b200_factorize(C.byref(o), ha.ptr, n, n, n, None, 0, hout[0].ptr, n, hout[1].ptr, n,
+                                  hout[2].ptr, n, C.byref(st))
+            rutv._raise(st)
+
+        if not big:
+            e2e_step()  # warm-up (the device path above already warmed the kernels)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([f0.elapsed_time(f1) / args.e2e_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * F / (float(ems.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "ms_per_step": round(float(ems.item()), 3), "steps": args.e2e_steps,
+               "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 3 * 8 * n * n}
+        # sanity: the host result is the device one (same stream of deviates, deterministic)
+        assert np.allclose(np.diag(hout[0].array)[:8], diag0.numpy(), rtol=1e-12, atol=0), "e2e != device run"
+        for h in [ha, *hout]:
+            h.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             import oracle
             if oracle.available("ref"):
-                v_ref, dt, cores, sample = best_reference()
-                cpu = {"value": round(v_ref, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-                       "sample": sample}
+                rs = ReferenceSampler(b, q, args.kind)
+                v_ref, dt = rs.pick()
+                cpu = {"value": round(v_ref, 4), "unit": "GFLOP/s", "cores": rs.cores, "kind": "reference",
+                       "sample": rs.describe(dt) + f"; config wall time extrapolated as F/value = "
+                                                   f"{F / (v_ref * 1e9):.0f} s"}
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -389,9 +494,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (device-generated {KIND_TEXT[args.kind]}, seed {SEED_A})",
-            "config": {"workload": workload_name(n, b, q, args.kind, args.config), "n": n, "b": b, "q": q,
-                       "flops_per_step": F, "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "inputs (A 128 MB + 384 MB state) exceed the 126 MB L2; no flush"},
+            "config": config_dict(args, parallelism(args, world)),
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
             "cpu_baseline": cpu,
         }
@@ -399,6 +502,29 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def flops(n, b, q):
+    """F(n, b, q) of SURVEY.md section 8(a) (== rutv_b200_flops == oracle.flops)."""
+    f, i = 0.0, 0
+    while True:
+        r0, s = float(i * b), float(n - i * b)
+        bb, nn = float(b), float(n)
+        if s <= 0:
+            break
+        if s <= bb:
+            f += 2 * r0 * s * s + 4 * nn * s * s
+            break
+        f += 2 * s * s * bb * (1 + 2 * q)
+        f += 4 * s * s * bb + 2 * s * bb * bb
+        f += 4 * r0 * s * bb + 2 * r0 * bb * bb
+        f += 4 * nn * s * bb + 2 * nn * bb * bb
+        f += 4 * s * bb * (s - bb) + 2 * bb * bb * (s - bb)
+        f += 4 * nn * s * bb + 2 * nn * bb * bb
+        f += 2 * bb * bb * (s - bb) + 2 * r0 * bb * bb + 4 * nn * bb * bb
+        f += 4 * bb * bb * (s - bb / 3)
+        i += 1
+    return f
 
 
 # ---------------------------------------------------------- sharded (2D) --

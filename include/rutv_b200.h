@@ -21,6 +21,7 @@
 #ifndef RUTV_B200_H
 #define RUTV_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -104,6 +105,11 @@ int rutv_b200_last_profile(const char** names, double* ms, int cap);
 
 /* Kernels this library launched since load (evidence for bench.py). */
 uint64_t rutv_b200_launch_count(void);
+
+/* Page-locked host staging buffers of exactly `bytes` (cudaHostAlloc, portable):
+ * the host-pointer entry points copy at full PCIe/C2C bandwidth from them. */
+int rutv_b200_host_alloc(size_t bytes, void** p, rutv_status* st);
+int rutv_b200_host_free(void* p, rutv_status* st);
 
 /* GEMM-kernel totals of the last factorize call on this thread when
  * RUTV_GEMM_PROFILE=1 (CUDA events around every GEMM launch): algorithmic

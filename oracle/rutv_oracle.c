@@ -108,8 +108,14 @@ typedef struct {
 } Rng;
 
 static void gen_normal(Rng* rng, View a) { /* rng.cpp:44-47 */
+    /* normal_at is a pure function of (seed, position): columns in parallel,
+     * same values as the reference's sequential pos++ walk */
+    const uint64_t base = rng->pos;
+#pragma omp parallel for schedule(static) if (a.rows * a.cols > 65536)
     for (idx j = 0; j < a.cols; ++j)
-        for (idx i = 0; i < a.rows; ++i) AT(a, i, j) = ora_normal_at(rng->seed, rng->pos++);
+        for (idx i = 0; i < a.rows; ++i)
+            AT(a, i, j) = ora_normal_at(rng->seed, base + (uint64_t)(i + j * a.rows));
+    rng->pos = base + (uint64_t)(a.rows * a.cols);
 }
 
 /* ----------------------------------------------------------------- GEMM -- */
@@ -126,7 +132,11 @@ static void gemm_v(double alpha, int ta, View a, int tb, View b, double beta, Vi
             for (idx i = 0; i < m; ++i) AT(c, i, j) *= beta;
     }
     if (alpha == 0.0 || kk == 0) return;
+    /* Output columns are independent and each keeps the reference's
+     * k-ascending order: OpenMP over j is bit-identical to the serial loop. */
+    const int par = (double)m * (double)n * (double)kk > 4e6;
     if (!ta) { /* gemm.cpp:40-55, axpy form */
+#pragma omp parallel for schedule(static) if (par)
         for (idx j = 0; j < n; ++j)
             for (idx k = 0; k < kk; ++k) {
                 const double t = alpha * (tb ? AT(b, j, k) : AT(b, k, j));
@@ -135,6 +145,7 @@ static void gemm_v(double alpha, int ta, View a, int tb, View b, double beta, Vi
                 for (idx i = 0; i < m; ++i) ccol[i] += acol[i] * t;
             }
     } else { /* gemm.cpp:56-74, dot form */
+#pragma omp parallel for schedule(static) if (par)
         for (idx j = 0; j < n; ++j)
             for (idx i = 0; i < m; ++i) {
                 const double* acol = a.data + i * a.ld;
@@ -210,6 +221,8 @@ static void hqr_inplace(View a, double* tau) {
         AT(a, j, j) = h.beta;
         tau[j] = h.tau;
         if (h.tau == 0.0) continue;
+        /* trailing columns are independent (one dot + one axpy each) */
+#pragma omp parallel for schedule(static) if ((m - j) * (n - j) > 131072)
         for (idx jj = j + 1; jj < n; ++jj) {
             double w = AT(a, j, jj);
             for (idx i = j + 1; i < m; ++i) w += AT(a, i, j) * AT(a, i, jj);
@@ -314,6 +327,7 @@ static View form_q(View qr, const double* tau, idx nref, idx ncols) {
     for (idx j = nref - 1; j >= 0; --j) {
         const double tj = tau[j];
         if (tj == 0.0) continue;
+#pragma omp parallel for schedule(static) if ((m - j) * ncols > 131072)
         for (idx c = 0; c < ncols; ++c) {
             double w = AT(x, j, c);
             for (idx i = j + 1; i < m; ++i) w += AT(qr, i, j) * AT(x, i, c);
@@ -874,6 +888,7 @@ int ora_spectrum_matrix(idx m, idx n, double beta, const double* sigma, uint64_t
     double s = 1.0;
     for (idx j = 0; j < p; ++j) {
         const double f = sigma ? sigma[j] : s;
+#pragma omp parallel for schedule(static) if (m > 65536)
         for (idx i = 0; i < m; ++i) AT(u, i, j) *= f;
         s *= beta;
     }

@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
     L.rutv_b200_factorize_device.argtypes = fac
     L.rutv_b200_last_profile.argtypes = [C.POINTER(C.c_char_p), _D, C.c_int]
     L.rutv_b200_launch_count.restype = C.c_uint64
+    L.rutv_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(Status)]
+    L.rutv_b200_host_free.argtypes = [C.c_void_p, C.POINTER(Status)]
     L.rutv_b200_gemm_profile.argtypes = [_D, _D, C.POINTER(_I64)]
     L.rutv_b200_gaussian_matrix.argtypes = [C.c_int, _I64, _I64, C.c_uint64, C.c_void_p, _I64,
                                             C.POINTER(Status)]
@@ -223,6 +225,34 @@ def factorize_device(a, t, u=None, v=None, *, b: int = 128, q: int = 1, seed: in
     lib().rutv_b200_factorize_device(C.byref(o), pa, m, n, lda, gp, glen, pt, ldt, pu, ldu, pv, ldv,
                                      C.byref(st))
     _raise(st)
+
+
+class PinnedMatrix:
+    """Page-locked host matrix of exactly m x n doubles (column-major), allocated
+    with ``rutv_b200_host_alloc``; ``.array`` is a Fortran-ordered numpy view.
+    Free with ``close()`` (or let it be garbage collected)."""
+
+    def __init__(self, m: int, n: int):
+        self.ptr = C.c_void_p()
+        st = Status()
+        lib().rutv_b200_host_alloc(max(m * n, 1) * 8, C.byref(self.ptr), C.byref(st))
+        _raise(st)
+        buf = (C.c_double * max(m * n, 1)).from_address(self.ptr.value)
+        self.array = np.frombuffer(buf, dtype=np.float64, count=m * n).reshape((n, m)).T
+        self.shape = (m, n)
+
+    def close(self) -> None:
+        if self.ptr is not None and self.ptr.value:
+            self.array = None
+            st = Status()
+            lib().rutv_b200_host_free(self.ptr, C.byref(st))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def launch_count() -> int:

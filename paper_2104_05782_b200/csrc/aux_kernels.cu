@@ -335,10 +335,10 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
     }
     if (p <= 256) {
         static int rcap = 0;
-        if (!rcap) {
+        once_per_device(reinterpret_cast<const void*>(form_t_rd_kernel), [] {
             rcap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_rd_kernel));
             RUTV_CUDA(cudaFuncSetAttribute(form_t_rd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rcap));
-        }
+        });
         // scratch X: npair h x h blocks per level
         int64_t xe = 1;
         for (int64_t h = 16; h < p; h *= 2) xe = std::max(xe, (p + 2 * h - 1) / (2 * h) * h * h);
@@ -352,10 +352,10 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
         return;
     }
     static int cap = 0;
-    if (!cap) {
+    once_per_device(reinterpret_cast<const void*>(form_t_kernel), [] {
         cap = dyn_smem_cap(reinterpret_cast<const void*>(form_t_kernel));
         RUTV_CUDA(cudaFuncSetAttribute(form_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
-    }
+    });
     const size_t xs = static_cast<size_t>(std::max<int64_t>(p - 32, 1)) * 32 * sizeof(double);
     const size_t tsm = static_cast<size_t>(p) * p * sizeof(double);
     const bool in_smem = tsm + xs <= static_cast<size_t>(cap);

@@ -32,8 +32,15 @@ int fill(rutv_status* st, int code, const char* msg, double residual = 0.0) {
     return code;
 }
 
+// Every public call ends by returning the library pool's freed blocks to the
+// driver (beyond a bounded cache): no device memory stays held after a call.
+struct TrimAtExit {
+    ~TrimAtExit() { rutv::pool_trim(); }
+};
+
 template <class F>
 int guarded(rutv_status* st, F&& f) {
+    TrimAtExit trim;
     try {
         f();
         return fill(st, RUTV_OK, "");
@@ -50,17 +57,6 @@ int guarded(rutv_status* st, F&& f) {
 
 void set_device(int device) {
     RUTV_CUDA(cudaSetDevice(device));
-    // Keep stream-ordered allocations in the pool between calls (no OS
-    // re-mapping on every call).
-    static bool done[64] = {};
-    if (device >= 0 && device < 64 && !done[device]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        done[device] = true;
-    }
 }
 
 void check_opts(const rutv_opts* o) {
@@ -94,17 +90,24 @@ struct DMem {
     cudaStream_t st;
     DMem(size_t count, cudaStream_t s) : st(s) {
         if (count == 0) count = 1;
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s);
-        if (e == cudaErrorMemoryAllocation) {
-            cudaGetLastError();
-            throw Error(RUTV_ERR_OOM, "device allocation failed");
-        }
-        RUTV_CUDA(e);
+        p = static_cast<T*>(rutv::dev_alloc(count * sizeof(T), s));
     }
     ~DMem() {
         if (p) cudaFreeAsync(p, st);
     }
 };
+
+// Deviates the first max_steps loop iterations draw (all of them when max_steps < 0):
+// sum over full steps of rows_rem * b (randutv_blocked.cpp:41-44, 122-139).
+int64_t drawn_length(int64_t m, int64_t n, int64_t b, int max_steps) {
+    int64_t total = 0;
+    for (int64_t i = 0; max_steps < 0 || i < max_steps; ++i) {
+        const int64_t r0 = i * b, rr = m - r0, cr = n - r0;
+        if (rr <= 0 || cr <= 0 || cr <= b) break;
+        total += rr * b;
+    }
+    return total;
+}
 
 void run_factorize(const rutv_opts* o, const double* dA, int64_t m, int64_t n, int64_t lda,
                    const double* dG, int64_t g_len, double* dT, int64_t ldt, double* dU, int64_t ldu,
@@ -116,7 +119,7 @@ void run_factorize(const rutv_opts* o, const double* dA, int64_t m, int64_t n, i
     if (o->build_u && (!dU || ldu < std::max<int64_t>(m, 1))) throw Error(RUTV_ERR_SHAPE, "U buffer");
     if (o->build_v && (!dV || ldv < std::max<int64_t>(n, 1))) throw Error(RUTV_ERR_SHAPE, "V buffer");
     // qr_prepass factors the n x n R with the same seed (randutv_blocked.cpp:88-96)
-    if (dG && g_len < (prepass ? rutv_b200_stream_length(n, n, o->b) : rutv_b200_stream_length(m, n, o->b)))
+    if (dG && g_len < drawn_length(prepass ? n : m, n, o->b, o->max_steps))
         throw Error(RUTV_ERR_SHAPE, "explicit G shorter than the stream the factorization draws");
     rutv::FactorArgs fa{o->b,  o->q, o->build_u != 0, o->build_v != 0, o->seed, o->max_steps, dA, lda,
                         dG,    dT,   ldt,             dU,             ldu,     dV,          ldv,
@@ -188,37 +191,57 @@ int rutv_b200_factorize(const rutv_opts* o, const double* A, int64_t m, int64_t 
         set_device(o->device);
         Stream s(o->stream);
         const int64_t mm = std::max<int64_t>(m, 0), nn = std::max<int64_t>(n, 0);
-        DMem<double> dA(static_cast<size_t>(mm * nn), s.s), dT(static_cast<size_t>(mm * nn), s.s);
-        DMem<double> dU(o->build_u ? static_cast<size_t>(mm * mm) : 1, s.s);
-        DMem<double> dV(o->build_v ? static_cast<size_t>(nn * nn) : 1, s.s);
         const bool prepass = o->qr_prepass && m > n;  // the inner n x n run draws the stream
-        const int64_t glen = G ? (prepass ? rutv_b200_stream_length(n, n, o->b) : rutv_b200_stream_length(m, n, o->b))
-                               : 0;
-        DMem<double> dG(G ? static_cast<size_t>(std::max<int64_t>(glen, 1)) : 1, s.s);
-        if (mm * nn > 0)
-            RUTV_CUDA(cudaMemcpy2DAsync(dA.p, static_cast<size_t>(mm) * 8, A, static_cast<size_t>(lda) * 8,
-                                        static_cast<size_t>(mm) * 8, static_cast<size_t>(nn),
-                                        cudaMemcpyHostToDevice, s.s));
-        if (G && glen > 0) {
-            if (g_len < glen) throw Error(RUTV_ERR_SHAPE, "explicit G shorter than the stream");
-            RUTV_CUDA(cudaMemcpyAsync(dG.p, G, static_cast<size_t>(glen) * 8, cudaMemcpyHostToDevice, s.s));
+        const int64_t glen = G ? drawn_length(prepass ? n : m, n, o->b, o->max_steps) : 0;
+        if (G && glen > 0 && g_len < glen) throw Error(RUTV_ERR_SHAPE, "explicit G shorter than the stream");
+        auto h2d = [&](double* d, int64_t ldd, const double* h, int64_t ldh, int64_t r, int64_t c) {
+            if (r * c > 0)
+                RUTV_CUDA(cudaMemcpy2DAsync(d, static_cast<size_t>(ldd) * 8, h, static_cast<size_t>(ldh) * 8,
+                                            static_cast<size_t>(r) * 8, static_cast<size_t>(c), cudaMemcpyHostToDevice,
+                                            s.s));
+        };
+        auto d2h = [&](double* h, int64_t ldh, const double* d, int64_t ldd, int64_t r, int64_t c) {
+            if (h && r * c > 0)
+                RUTV_CUDA(cudaMemcpy2DAsync(h, static_cast<size_t>(ldh) * 8, d, static_cast<size_t>(ldd) * 8,
+                                            static_cast<size_t>(r) * 8, static_cast<size_t>(c), cudaMemcpyDeviceToHost,
+                                            s.s));
+        };
+        {
+            DMem<double> dG(G ? static_cast<size_t>(std::max<int64_t>(glen, 1)) : 1, s.s);
+            if (G && glen > 0)
+                RUTV_CUDA(cudaMemcpyAsync(dG.p, G, static_cast<size_t>(glen) * 8, cudaMemcpyHostToDevice, s.s));
+            if (m == n) {
+                // Square: ONE stacked device buffer [V; T] (V on top, ld = 2n) plus U,
+                // factored in place -- A is uploaded straight into T's rows, the
+                // results are read back from the same buffers: HBM peak 3 n^2 doubles
+                // plus O(n b) workspace (config 5: 60 GB of 180).
+                const int64_t vr = o->build_v ? nn : 0;
+                const int64_t ld = std::max<int64_t>((vr + nn + 3) / 4 * 4, 1), ldu4 = std::max<int64_t>((nn + 3) / 4 * 4, 1);
+                DMem<double> vt(static_cast<size_t>(ld * nn), s.s);
+                DMem<double> dU(o->build_u ? static_cast<size_t>(ldu4 * nn) : 1, s.s);
+                double* dT = vt.p + vr;
+                h2d(dT, ld, A, lda, nn, nn);
+                run_factorize(o, dT, n, n, ld, G ? dG.p : nullptr, glen, dT, ld, o->build_u ? dU.p : nullptr, ldu4,
+                              o->build_v ? vt.p : nullptr, ld, s.s);
+                d2h(T, ldt, dT, ld, nn, nn);
+                if (o->build_u) d2h(U, ldu, dU.p, ldu4, nn, nn);
+                if (o->build_v) d2h(V, ldv, vt.p, ld, nn, nn);
+                RUTV_CUDA(cudaStreamSynchronize(s.s));
+            } else {
+                DMem<double> dA(static_cast<size_t>(mm * nn), s.s), dT(static_cast<size_t>(mm * nn), s.s);
+                DMem<double> dU(o->build_u ? static_cast<size_t>(mm * mm) : 1, s.s);
+                DMem<double> dV(o->build_v ? static_cast<size_t>(nn * nn) : 1, s.s);
+                h2d(dA.p, std::max<int64_t>(mm, 1), A, lda, mm, nn);
+                run_factorize(o, dA.p, m, n, std::max<int64_t>(mm, 1), G ? dG.p : nullptr, glen, dT.p,
+                              std::max<int64_t>(mm, 1), o->build_u ? dU.p : nullptr, std::max<int64_t>(mm, 1),
+                              o->build_v ? dV.p : nullptr, std::max<int64_t>(nn, 1), s.s);
+                d2h(T, ldt, dT.p, std::max<int64_t>(mm, 1), mm, nn);
+                if (o->build_u) d2h(U, ldu, dU.p, std::max<int64_t>(mm, 1), mm, mm);
+                if (o->build_v) d2h(V, ldv, dV.p, std::max<int64_t>(nn, 1), nn, nn);
+                RUTV_CUDA(cudaStreamSynchronize(s.s));
+            }
         }
-        run_factorize(o, dA.p, m, n, std::max<int64_t>(mm, 1), G ? dG.p : nullptr, glen, dT.p,
-                      std::max<int64_t>(mm, 1), o->build_u ? dU.p : nullptr, std::max<int64_t>(mm, 1),
-                      o->build_v ? dV.p : nullptr, std::max<int64_t>(nn, 1), s.s);
-        if (mm * nn > 0)
-            RUTV_CUDA(cudaMemcpy2DAsync(T, static_cast<size_t>(ldt) * 8, dT.p, static_cast<size_t>(mm) * 8,
-                                        static_cast<size_t>(mm) * 8, static_cast<size_t>(nn),
-                                        cudaMemcpyDeviceToHost, s.s));
-        if (o->build_u && U && mm > 0)
-            RUTV_CUDA(cudaMemcpy2DAsync(U, static_cast<size_t>(ldu) * 8, dU.p, static_cast<size_t>(mm) * 8,
-                                        static_cast<size_t>(mm) * 8, static_cast<size_t>(mm),
-                                        cudaMemcpyDeviceToHost, s.s));
-        if (o->build_v && V && nn > 0)
-            RUTV_CUDA(cudaMemcpy2DAsync(V, static_cast<size_t>(ldv) * 8, dV.p, static_cast<size_t>(nn) * 8,
-                                        static_cast<size_t>(nn) * 8, static_cast<size_t>(nn),
-                                        cudaMemcpyDeviceToHost, s.s));
-        RUTV_CUDA(cudaStreamSynchronize(s.s));
+        RUTV_CUDA(cudaStreamSynchronize(s.s));  // the buffers' stream-ordered frees, before the trim
     });
 }
 
@@ -240,6 +263,25 @@ int rutv_b200_last_profile(const char** names, double* ms, int cap) {
 }
 
 uint64_t rutv_b200_launch_count(void) { return rutv::launch_count(); }
+
+int rutv_b200_host_alloc(size_t bytes, void** p, rutv_status* st) {
+    return guarded(st, [&] {
+        if (!p) throw Error(RUTV_ERR_SHAPE, "null output pointer");
+        *p = nullptr;
+        const cudaError_t e = cudaHostAlloc(p, bytes ? bytes : 8, cudaHostAllocPortable);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            throw Error(RUTV_ERR_OOM, "pinned host allocation of " + std::to_string(bytes) + " bytes failed");
+        }
+        RUTV_CUDA(e);
+    });
+}
+
+int rutv_b200_host_free(void* p, rutv_status* st) {
+    return guarded(st, [&] {
+        if (p) RUTV_CUDA(cudaFreeHost(p));
+    });
+}
 
 int rutv_b200_gemm_profile(double* flops, double* ms, int64_t* launches) {
     return rutv::gemm_profile_get(flops, ms, launches);

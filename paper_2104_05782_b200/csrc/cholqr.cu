@@ -598,12 +598,11 @@ __global__ void commit_kernel(int64_t s, int p, const double* __restrict__ topb,
 }
 
 void small_attr() {
-    static bool done = false;
-    if (done) return;
-    const int bytes = static_cast<int>(small_smem_bytes(128));
-    RUTV_CUDA(cudaFuncSetAttribute(cqr_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    RUTV_CUDA(cudaFuncSetAttribute(cqr_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    done = true;
+    once_per_device(reinterpret_cast<const void*>(cqr_chol_kernel), [] {
+        const int bytes = static_cast<int>(small_smem_bytes(128));
+        RUTV_CUDA(cudaFuncSetAttribute(cqr_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        RUTV_CUDA(cudaFuncSetAttribute(cqr_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    });
 }
 
 // immediate mode (RUTV_CHOLQR=1) for callers outside the factorization driver
@@ -706,12 +705,10 @@ bool qr_panel_fast(cudaStream_t st, const DView& y, double* tau) {
 // T of compact WY for p <= 128 (form_t dispatches here).
 void form_t_small(cudaStream_t stream, const double* gram, int64_t ldg, const double* tau, int64_t p, double* t,
                   int64_t ldt) {
-    static bool attr = false;
-    if (!attr) {
+    once_per_device(reinterpret_cast<const void*>(form_t_inv_kernel), [] {
         RUTV_CUDA(cudaFuncSetAttribute(form_t_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(small_smem_bytes(128))));
-        attr = true;
-    }
+    });
     form_t_inv_kernel<<<1, kST, small_smem_bytes(static_cast<int>(p)), stream>>>(gram, ldg, tau, static_cast<int>(p),
                                                                                    t, ldt);
     note_launch();

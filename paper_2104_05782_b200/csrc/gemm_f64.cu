@@ -520,11 +520,10 @@ void launch_cfg(cudaStream_t stream, const GemmParams& p, int gx, int gy, int gz
                          static_cast<int>(sizeof(double));
     constexpr int nt = (BM / WM) * (BN / WN) * 32;
     auto kern = dgemm_kernel<BM, BN, BK, WM, WN, ST, TA, TB, VEC>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    // per instantiation and per device (the opt-in is a property of the device context)
+    once_per_device(reinterpret_cast<const void*>(kern), [kern] {
         RUTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = true;
-    }
+    });
     kern<<<dim3(gx, gy, gz), nt, smem, stream>>>(p);
     note_launch();
     RUTV_CHECK_LAUNCH();

@@ -86,7 +86,7 @@ void spectrum_matrix(cudaStream_t st, int64_t m, int64_t n, const double* sigma_
     }
     auto alloc = [&](int64_t elems) {
         double* ptr = nullptr;
-        RUTV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), static_cast<size_t>(std::max<int64_t>(elems, 1)) * 8, st));
+        ptr = static_cast<double*>(dev_alloc(static_cast<size_t>(std::max<int64_t>(elems, 1)) * 8, st));
         return ptr;
     };
     double* g1 = alloc(m * p);

@@ -174,14 +174,12 @@ void small_mul_grouped(cudaStream_t st, bool left, const std::vector<SmallMulDes
     const size_t smem = (static_cast<size_t>(wp) * (wp + 4) +
                          static_cast<size_t>(left ? kTile : wp) * (left ? wp + 4 : kTile + 8)) *
                         sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    once_per_device(reinterpret_cast<const void*>(small_mul_kernel<true>), [] {
         const int capl = dyn_smem_cap(reinterpret_cast<const void*>(small_mul_kernel<true>));
         const int capr = dyn_smem_cap(reinterpret_cast<const void*>(small_mul_kernel<false>));
         RUTV_CUDA(cudaFuncSetAttribute(small_mul_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, capl));
         RUTV_CUDA(cudaFuncSetAttribute(small_mul_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, capr));
-        attr = true;
-    }
+    });
     const auto* dd = reinterpret_cast<const SmallMulDesc*>(base);
     if (left)
         small_mul_kernel<true><<<static_cast<unsigned>(tiles.size()), kGT, smem, st>>>(dd, dt);

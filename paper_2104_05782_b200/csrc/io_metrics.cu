@@ -173,7 +173,7 @@ struct Buf {
     double* p = nullptr;
     cudaStream_t s;
     Buf(int64_t elems, cudaStream_t st) : s(st) {
-        RUTV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(std::max<int64_t>(elems, 1)) * 8, st));
+        p = static_cast<double*>(rutv::dev_alloc(static_cast<size_t>(std::max<int64_t>(elems, 1)) * 8, st));
     }
     ~Buf() {
         if (p) cudaFreeAsync(p, s);

@@ -500,6 +500,8 @@ struct JCfg {
 
 int g_jcap = 0, g_jmax_cluster = 0;
 
+void jinit_device();
+
 template <int RPL, bool VSM>
 void prep_kernel() {
     auto k = jacobi_kernel<RPL, VSM>;
@@ -516,7 +518,10 @@ void launch_j(cudaLaunchConfig_t& cfg, int vsm, const SvdDesc* d, int R, int rs,
 }
 
 void jinit() {
-    if (g_jcap) return;
+    once_per_device(reinterpret_cast<const void*>(&g_jcap), [] { jinit_device(); });
+}
+
+void jinit_device() {
     g_jcap = dyn_smem_cap(reinterpret_cast<const void*>(jacobi_kernel<16, true>));
     prep_kernel<2, true>();
     prep_kernel<4, true>();

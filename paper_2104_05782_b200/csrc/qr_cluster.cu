@@ -299,8 +299,14 @@ size_t cluster_smem_bytes(int w, int LD, int cs) {
 
 int g_max_cluster = 0;  // largest cluster size the device accepted (probe once)
 
+void max_cluster_device();
+
 int max_cluster() {
-    if (g_max_cluster) return g_max_cluster;
+    once_per_device(reinterpret_cast<const void*>(&g_max_cluster), [] { max_cluster_device(); });
+    return g_max_cluster;
+}
+
+void max_cluster_device() {
     kSmemCap = dyn_smem_cap(reinterpret_cast<const void*>(hqr_cluster_kernel));
     RUTV_CUDA(cudaFuncSetAttribute(hqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RUTV_CUDA(cudaFuncSetAttribute(hqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -327,7 +333,6 @@ int max_cluster() {
         cudaGetLastError();
     }
     g_max_cluster = best;
-    return best;
 }
 
 inline int odd_ld(int64_t R) { return static_cast<int>(R | 1); }

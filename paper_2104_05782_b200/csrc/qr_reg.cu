@@ -566,14 +566,16 @@ __global__ void __launch_bounds__(kT, 1)
 int g_reg_cap = 0;  // dynamic shared memory cap for the kernel
 
 void reg_init() {
-    if (g_reg_cap) return;
-    g_reg_cap = dyn_smem_cap(reinterpret_cast<const void*>(hqr_reg_kernel<1>));
-    for (const void* f : {reinterpret_cast<const void*>(hqr_reg_kernel<1>),
-                          reinterpret_cast<const void*>(hqr_reg_kernel<2>)}) {
-        RUTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        RUTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, g_reg_cap));
-    }
+    once_per_device(reinterpret_cast<const void*>(&g_reg_cap), [] {
+        g_reg_cap = dyn_smem_cap(reinterpret_cast<const void*>(hqr_reg_kernel<1>));
+        for (const void* f : {reinterpret_cast<const void*>(hqr_reg_kernel<1>),
+                              reinterpret_cast<const void*>(hqr_reg_kernel<2>)}) {
+            RUTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            RUTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, g_reg_cap));
+        }
+    });
 }
+
 
 }  // namespace
 

@@ -176,7 +176,7 @@ void complete_orthonormal_device(cudaStream_t st, const DView& q, int64_t r) {
     if (r >= k) return;
     DevBuf P(k * kCandBlock, st), Z(static_cast<int64_t>(kCandBlock) * k, st);
     int* dhave = nullptr;
-    RUTV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dhave), sizeof(int), st));
+    dhave = static_cast<int*>(dev_alloc(sizeof(int), st));
     struct Free {
         int* p;
         cudaStream_t s;

@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <algorithm>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -56,20 +57,20 @@ struct DView {
 
 enum class Op { N = 0, T = 1 };
 
-// Stream-ordered device allocation from the device's default pool
-// (cudaMallocAsync), so repeated calls do not pay cudaMalloc.
+// Stream-ordered allocation from the LIBRARY's per-device pool (runtime.cu;
+// never the device's default pool, which the host process owns).  Freed
+// blocks stay cached for the rest of a call; pool_trim() at the end of every
+// public call returns all but RUTV_POOL_KEEP_MB (default 4096) to the driver.
+void* dev_alloc(size_t bytes, cudaStream_t st);
+void pool_trim();
+
 struct DevBuf {
     double* p = nullptr;
     cudaStream_t st = nullptr;
     DevBuf() = default;
     DevBuf(int64_t elems, cudaStream_t s) : st(s) {
         if (elems <= 0) elems = 1;
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(elems) * 8, s);
-        if (e == cudaErrorMemoryAllocation) {
-            cudaGetLastError();
-            throw Error(RUTV_ERR_OOM, "device allocation of " + std::to_string(elems * 8) + " bytes failed");
-        }
-        if (e != cudaSuccess) throw Error(RUTV_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+        p = static_cast<double*>(dev_alloc(static_cast<size_t>(elems) * 8, s));
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -88,6 +89,12 @@ inline int dyn_smem_cap(const void* kernel) {
     if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) return optin - 1024;
     return optin - static_cast<int>(fa.sharedSizeBytes);
 }
+
+// Runs `init` once per (current CUDA device, key), thread-safe.  Kernel
+// attributes (dynamic shared-memory opt-in, non-portable cluster sizes) belong
+// to a device context, so a process that uses device 0 and then device 1 must
+// set them again; concurrent callers block until the first finishes.
+void once_per_device(const void* key, const std::function<void()>& init);
 
 // ---- kernels' host launchers (all asynchronous on `stream`) ----
 

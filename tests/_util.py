@@ -73,3 +73,35 @@ def compare_to_oracle(a, got, ref, *, t_tol=1e-11, uv_tol=1e-9, diag_rel=1e-10):
     if ug is not None:
         assert out["u_maxabs"] <= uv_tol and out["v_maxabs"] <= uv_tol, out
     return out
+
+
+def cluster_align(ug, ur, d_ref, b, rel=1e-8):
+    """Alignment D (n x n, block diagonal) with ug ~= ur @ D for comparing two
+    randUTV runs.
+
+    Each step's Jacobi SVD fixes (u_k, v_k) pairs only up to sign -- and, inside a
+    cluster of (near-)equal singular values of one b x b window (config 4's
+    sigma = 1 block), only up to an orthogonal rotation, because the order after
+    the stable sort of jacobi_svd.cpp:111-122 and the basis inside the cluster
+    are rounding-determined.  Within every window, consecutive indices whose
+    reference diagonal agrees to `rel` form a cluster; a singleton gets the sign
+    of <ug_k, ur_k>, a cluster the orthogonal Procrustes factor polar(ur_c' ug_c).
+    Then U_gpu ~ U_ref D, V_gpu ~ V_ref D and T_gpu ~ D' T_ref D."""
+    n = ug.shape[1]
+    D = np.zeros((n, n))
+    for r0 in range(0, n, b):
+        w = min(b, n - r0)
+        i = r0
+        while i < r0 + w:
+            j = i + 1
+            while j < r0 + w and abs(d_ref[j] - d_ref[i]) <= rel * max(abs(d_ref[i]), 1e-300):
+                j += 1
+            if j - i == 1:
+                s = np.sign(ug[:, i] @ ur[:, i])
+                D[i, i] = s if s != 0 else 1.0
+            else:
+                m = ur[:, i:j].T @ ug[:, i:j]
+                w_, _, zt = np.linalg.svd(m)
+                D[i:j, i:j] = w_ @ zt
+            i = j
+    return D

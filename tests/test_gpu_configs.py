@@ -1,12 +1,27 @@
-"""BASELINE.json configs on the B200: parity with the oracle where the oracle
-finishes, size-independent invariants everywhere (test_randutv_blocked.cpp:40-78).
+"""Every BASELINE.json config on the B200 at north_star tolerances.
 
-  config 1  n=2000  b=128 q=0 Gaussian   full oracle run (~30 s CPU), entrywise parity
-  config 2  n=4000  b=128 q=2 geometric  first-step oracle parity + invariants + diag vs sigma
-  config 3  n=10000 b=256 q=1 Gaussian   invariants (orthogonality, residual, structure)
-  config 5  n=50000 b=512 q=2 Gaussian   first two steps (max_steps), invariants of the partial factors
-Checks of UTV products run with torch on the GPU (verification only).
+  config 1  n=2000  b=128 q=0 Gaussian   full oracle run, entrywise parity (sign-aligned)
+  config 2  n=4000  b=128 q=2 geometric  full run vs the UNMODIFIED reference's own full run
+                                          (tests/golden/config2_ref.npz, made by
+                                          tests/golden/make_config_fixtures.py): diag(T) under the
+                                          mixed tolerance of SURVEY 8a.3, sampled T / U / V entries,
+                                          diag vs sigma against the reference's own quality
+  config 3  n=10000 b=256 q=1 Gaussian   first step vs the reference's step API
+                                          (tests/golden/config3_step1_ref.npz) + full-run invariants
+  config 4  n=30000 b=256 q=2 cliff      full run: residual, orthogonality, structure, sigma(T) and
+                                          diag(T) against the constructed spectrum
+  config 5  n=50000 b=512 q=2 Gaussian   full run: residual, orthogonality, structure
+
+Invariants follow test_randutv_blocked.cpp:40-78 and acceptance.cpp:91-165.  Orthogonality
+is reported in three norms: the north_star's 1e-12 is asserted in the
+max-entry and spectral norms; the Frobenius norm is held to the reference's own budget
+100 max(m, n) eps (acceptance.cpp:101) and reported next to the reference's value where
+the reference ran on the same input.  Products for the checks run with torch on the GPU
+(verification only); A, T, U, V are factored in place in HBM (stacked [V; T]).
 """
+import hashlib
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -17,34 +32,98 @@ from tests._util import check_structure, compare_to_oracle
 
 pytestmark = pytest.mark.gpu
 
+EPS = float(np.finfo(np.float64).eps)
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
 
 def _cm(m, n):
     return torch.empty((n, m), dtype=torch.float64, device="cuda").T
 
 
-def _device_run(a, b, q, seed, g=None, max_steps=-1):
+def _run(a, b, q, seed, g=None, max_steps=-1):
+    """In-place factorization: T and V share one stacked device buffer."""
     n = a.shape[0]
-    t, u, v = _cm(n, n), _cm(n, n), _cm(n, n)
+    vt = _cm(2 * n, n)
+    t, v = vt[n:, :], vt[:n, :]
+    u = _cm(n, n)
     rutv.factorize_device(a, t, u, v, b=b, q=q, seed=seed, g=g, max_steps=max_steps)
     return t, u, v
 
 
-def _invariants(a, t, u, v, b, full=True, resid_tol=1e-12, orth_tol=1e-11):
+def _residual(a, t, u, v, blk=4096):
+    """||A - U T V'||_F / ||A||_F in column blocks (bounded temporaries at n = 50000)."""
+    n = a.shape[1]
+    acc = 0.0
+    for j0 in range(0, n, blk):
+        j1 = min(n, j0 + blk)
+        e = a[:, j0:j1] - u @ (t @ v[j0:j1, :].T)
+        acc += float(torch.sum(e * e).item())
+        del e
+    return acc ** 0.5 / torch.linalg.norm(a).item()
+
+
+def _sym_spec_norm(e, iters=100):
+    """Largest |eigenvalue| of a symmetric matrix by power iteration (a lower bound that
+    converges to ||E||_2)."""
+    g = torch.Generator(device=e.device).manual_seed(7)
+    x = torch.randn(e.shape[0], 1, dtype=e.dtype, device=e.device, generator=g)
+    x /= torch.linalg.norm(x)
+    lam = 0.0
+    for _ in range(iters):
+        y = e @ x
+        lam = float(torch.linalg.norm(y).item())
+        if lam == 0.0:
+            return 0.0
+        x = y / lam
+    return lam
+
+
+def _orth(q):
+    """(Frobenius, max-entry, spectral) norms of Q'Q - I."""
+    e = q.T @ q
+    e.diagonal().sub_(1.0)
+    out = (float(torch.linalg.norm(e).item()), float(e.abs().max().item()), _sym_spec_norm(e))
+    del e
+    return out
+
+
+def _structure_gpu(t, b):
+    """test_randutv_blocked.cpp:52-66 on the device: strictly-lower T exact zeros,
+    every b x b diagonal window exactly diagonal, non-increasing, >= 0."""
+    n = t.shape[1]
+    for j0 in range(0, n, 4096):
+        j1 = min(n, j0 + 4096)
+        blk = t[:, j0:j1]
+        rows = torch.arange(n, device=t.device)[:, None]
+        cols = torch.arange(j0, j1, device=t.device)[None, :]
+        assert int(torch.count_nonzero(blk.masked_fill(rows <= cols, 0.0)).item()) == 0, "strictly-lower T != 0"
+    for r0 in range(0, n, b):
+        w = min(b, n - r0)
+        win = t[r0:r0 + w, r0:r0 + w]
+        d = torch.diagonal(win)
+        assert int(torch.count_nonzero(win - torch.diag(d)).item()) == 0, f"window {r0} not diagonal"
+        assert bool(torch.all(d[:-1] >= d[1:]).item()) and float(d[-1].item()) >= 0.0, f"window {r0}"
+
+
+def _invariants(a, t, u, v, b, label):
     n = a.shape[0]
-    nf = torch.linalg.norm(a).item()
-    res = torch.linalg.norm(a - u @ t @ v.T).item() / nf
-    eye = torch.eye(n, dtype=torch.float64, device="cuda")
-    ou = torch.linalg.norm(u.T @ u - eye).item()
-    ov = torch.linalg.norm(v.T @ v - eye).item()
-    assert res < resid_tol, res
-    # reference budget 100 max(m,n) eps (acceptance.cpp:101) and the 1e-11 of test_randutv_blocked.cpp:48
-    assert ou < max(orth_tol, 100 * n * 2.2e-16) and ov < max(orth_tol, 100 * n * 2.2e-16), (ou, ov)
-    if full:
-        tt = t.cpu().numpy()
-        check_structure(np.asfortranarray(tt), b)
+    res = _residual(a, t, u, v)
+    ou, ov = _orth(u), _orth(v)
+    print(f"\n[{label}] resid {res:.3e}  U'U-I fro/max/2 {ou[0]:.3e}/{ou[1]:.3e}/{ou[2]:.3e}  "
+          f"V'V-I fro/max/2 {ov[0]:.3e}/{ov[1]:.3e}/{ov[2]:.3e}")
+    assert res <= 1e-12, res
+    for o in (ou, ov):
+        assert o[1] <= 1e-12 and o[2] <= 1e-12, o  # north_star 1e-12: max-entry and spectral norms
+        assert o[0] <= 100 * n * EPS, o  # the reference's budget in Frobenius (acceptance.cpp:101)
+    _structure_gpu(t, b)
     return res, ou, ov
 
 
+def _sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.asfortranarray(a).tobytes(order="F")).hexdigest()
+
+
+# ------------------------------------------------------------------------- config 1
 def test_config1_full_parity():
     n, b, q = 2000, 128, 0
     a = oracle.gaussian_matrix(n, n, 1)
@@ -52,65 +131,139 @@ def test_config1_full_parity():
     got = rutv.factorize(a, b=b, q=q, seed=2, g=g)
     ref = oracle.randutv(a, b=b, q=q, seed=2)
     check_structure(got[0], b)
-    out = compare_to_oracle(a, got, ref, t_tol=1e-11, uv_tol=1e-8, diag_rel=1e-10)
-    assert np.linalg.norm(a - got[1] @ got[0] @ got[2].T) / np.linalg.norm(a) < 1e-12, out
+    out = compare_to_oracle(a, got, ref, t_tol=1e-13, uv_tol=1e-11, diag_rel=1e-10)
+    t, u, v = got
+    res = np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a)
+    assert res < 1e-13, out
+    for mine, theirs in ((u, ref[1]), (v, ref[2])):
+        e, er = mine.T @ mine - np.eye(n), theirs.T @ theirs - np.eye(n)
+        fro, mx, sp = np.linalg.norm(e), np.abs(e).max(), np.linalg.norm(e, 2)
+        print(f"\n[config1] {out} orth fro/max/2 {fro:.3e}/{mx:.3e}/{sp:.3e} "
+              f"(reference {np.linalg.norm(er):.3e}/{np.abs(er).max():.3e}/{np.linalg.norm(er, 2):.3e})")
+        assert mx <= 1e-12 and sp <= 1e-12
+        assert fro <= max(2 * np.linalg.norm(er), 100 * n * EPS)
 
 
-def test_config2_geometric():
-    n, b, q = 4000, 128, 2
-    beta = 10 ** (-12 / (n - 1))
-    a = _cm(n, n)
-    rutv.spectrum_matrix_device(a, 1, beta=beta)
-    t, u, v = _device_run(a, b, q, 2)
-    _invariants(a, t, u, v, b)
-    # diag(T) vs sigma_i = beta^(i-1): a quality check, the reference itself only reaches
-    # max rel err ~0.18 here; require the same order
+# ------------------------------------------------------------------------- config 2
+def test_config2_full_vs_reference():
+    fx = np.load(os.path.join(GOLDEN, "config2_ref.npz"))
+    n, b, q = int(fx["n"]), int(fx["b"]), int(fx["q"])
+    ah = oracle.geometric_matrix(n, n, float(fx["beta"]), int(fx["seed_a"]))
+    assert _sha(ah) == str(fx["a_sha256"]), "regenerated A is not the reference run's input"
+    a = torch.from_numpy(np.ascontiguousarray(ah.T)).cuda().T
+    g = torch.from_numpy(oracle.normal_stream(int(fx["seed_g"]), 0, oracle.stream_length(n, n, b))).cuda()
+    t, u, v = _run(a, b, q, int(fx["seed_g"]), g=g)
+    res, ou, ov = _invariants(a, t, u, v, b, "config2")
+    print(f"[config2] reference on the same input: resid {float(fx['ref_resid_fro']):.3e}  "
+          f"U fro/max/2 {float(fx['ref_orth_u_fro']):.3e}/{float(fx['ref_orth_u_max']):.3e}/"
+          f"{float(fx['ref_orth_u_spec']):.3e}  V {float(fx['ref_orth_v_fro']):.3e}/"
+          f"{float(fx['ref_orth_v_max']):.3e}/{float(fx['ref_orth_v_spec']):.3e}")
+    # diag(T) vs the reference: mixed tolerance |dd| <= 1e-10 |d| + 10 eps sigma_1 (SURVEY 8a.3,
+    # calibrated on the reference against itself under 1-ulp input perturbation)
     d = torch.diagonal(t).cpu().numpy()
-    sig = beta ** np.arange(n)
-    assert np.max(np.abs(d[:2000] - sig[:2000]) / sig[:2000]) < 0.5
-    # first-step parity with the oracle on the same A (host copy) and the reference's G
-    ah = np.asfortranarray(a.cpu().numpy())
-    g = torch.from_numpy(oracle.normal_stream(2, 0, oracle.stream_length(n, n, b))).cuda()
-    t1, u1, v1 = _device_run(a, b, q, 2, g=g, max_steps=1)
-    tr, ur, vr = oracle.randutv(ah, b=b, q=q, seed=2, max_steps=1)
-    tg = t1.cpu().numpy()
-    # mixed tolerance of SURVEY 8a.3 on the finished diagonal block
-    dd = np.abs(np.diag(tg)[:b] - np.diag(tr)[:b])
-    assert np.all(dd <= 1e-10 * np.abs(np.diag(tr)[:b]) + 10 * 2.2e-16 * np.abs(tr[0, 0]) + 1e-12), dd.max()
-    nf = np.linalg.norm(ah)
-    ug = u1.cpu().numpy()
-    s = np.sign(np.einsum("ij,ij->j", ug[:, :b], ur[:, :b]))
-    assert np.max(np.abs(tg[:b, :b] - s[:, None] * tr[:b, :b] * s[None, :])) / nf < 1e-11
+    dr = fx["diag"]
+    dd = np.abs(d - dr)
+    tol = 1e-10 * np.abs(dr) + 10 * EPS * abs(dr[0])
+    pure = int(np.sum(dd > 1e-10 * np.abs(dr)))
+    print(f"[config2] diag: max |dd|/(tol) {np.max(dd / tol):.3e}; pure 1e-10-relative failures {pure} of {n} "
+          f"(the reference fails 1502 against itself, SURVEY 8a.3)")
+    assert np.all(dd <= tol), np.argmax(dd / tol)
+    # sign alignment from the sampled U rows; entrywise parity on the well-separated head
+    rows = fx["rows"]
+    ug, vg = u[rows, :].cpu().numpy(), v[rows, :].cpu().numpy()
+    s = np.sign(np.einsum("ij,ij->j", ug, fx["u_rows"]))
+    s[s == 0] = 1.0
+    head = 2000  # sigma >= 1e-6: the part of the spectrum where U / V entries are well determined
+    du = np.max(np.abs(ug[:, :head] * s[:head] - fx["u_rows"][:, :head]))
+    dv = np.max(np.abs(vg[:, :head] * s[:head] - fx["v_rows"][:, :head]))
+    ti, tj = fx["t_i"], fx["t_j"]
+    tg = t[torch.from_numpy(ti).cuda(), torch.from_numpy(tj).cuda()].cpu().numpy()
+    sel = (ti < head) & (tj < head)
+    nf = float(torch.linalg.norm(a).item())
+    dt = np.max(np.abs(tg[sel] * s[ti[sel]] * s[tj[sel]] - fx["t_val"][sel])) / nf
+    print(f"[config2] head (k < {head}) max|dU| {du:.3e} max|dV| {dv:.3e} max|dT|/||A|| {dt:.3e}")
+    assert du <= 1e-8 and dv <= 1e-8 and dt <= 1e-11
+    # diag(T) vs sigma: the reference's own quality on this input, not better than it
+    sig = float(fx["beta"]) ** np.arange(n)
+    mine, theirs = np.abs(d - sig) / sig, np.abs(dr - sig) / sig
+    print(f"[config2] diag vs sigma max rel: b200 {mine.max():.4f} (first half {mine[:n // 2].max():.4f}); "
+          f"reference {theirs.max():.4f} ({theirs[:n // 2].max():.4f})")
+    assert mine.max() <= theirs.max() + 1e-3 and mine[:n // 2].max() <= theirs[:n // 2].max() + 1e-3
 
 
-def test_config3_invariants():
+# ------------------------------------------------------------------------- config 3
+def test_config3_first_step_vs_reference():
+    fx = np.load(os.path.join(GOLDEN, "config3_step1_ref.npz"))
+    n, b, q = int(fx["n"]), int(fx["b"]), int(fx["q"])
+    ah = oracle.gaussian_matrix(n, n, int(fx["seed_a"]))
+    assert _sha(ah) == str(fx["a_sha256"])
+    a = torch.from_numpy(np.ascontiguousarray(ah.T)).cuda().T
+    del ah
+    g = torch.from_numpy(oracle.normal_stream(int(fx["seed_g"]), 0, n * b)).cuda()
+    t, u, v = _run(a, b, q, int(fx["seed_g"]), g=g, max_steps=1)
+    nf = float(fx["a_fro"])
+    d = torch.diagonal(t)[:b].cpu().numpy()
+    drel = np.max(np.abs(d - fx["diag"]) / np.abs(fx["diag"]))
+    rows = torch.from_numpy(fx["rows"]).cuda()
+    ug, vg = u[rows, :b].cpu().numpy(), v[rows, :b].cpu().numpy()
+    s = np.sign(np.einsum("ij,ij->j", ug, fx["u_rows"]))
+    s[s == 0] = 1.0
+    du = np.max(np.abs(ug * s - fx["u_rows"]))
+    dv = np.max(np.abs(vg * s - fx["v_rows"]))
+    strip = t[:b, torch.from_numpy(fx["strip_cols"]).cuda()].cpu().numpy()
+    dstrip = np.max(np.abs(strip * s[:, None] - fx["strip"])) / nf
+    t22 = t[torch.from_numpy(fx["t22_i"]).cuda(), torch.from_numpy(fx["t22_j"]).cuda()].cpu().numpy()
+    dt22 = np.max(np.abs(t22 - fx["t22_val"])) / nf
+    print(f"\n[config3 step 1] diag rel {drel:.3e} |dU| {du:.3e} |dV| {dv:.3e} strip {dstrip:.3e} "
+          f"T22 {dt22:.3e} (x ||A||_F)")
+    assert drel <= 1e-10  # north_star: diag(T) within 1e-10 relative (Gaussian: achievable as stated)
+    assert du <= 1e-11 and dv <= 1e-11
+    assert dstrip <= 1e-13 and dt22 <= 1e-13
+
+
+def test_config3_full_invariants():
     n, b, q = 10000, 256, 1
     a = _cm(n, n)
     rutv.gaussian_matrix_device(a, 1)
-    t, u, v = _device_run(a, b, q, 2)
-    _invariants(a, t, u, v, b, resid_tol=1e-12, orth_tol=1e-11)
-    # singular values of T equal those of A (test_randutv_blocked.cpp:71-78), checked on the
-    # diagonal's top block against torch's SVD of A
-    sa = torch.linalg.svdvals(a)
-    st = torch.linalg.svdvals(t)
-    assert torch.max(torch.abs(sa - st)).item() < 1e-11 * sa[0].item()
+    t, u, v = _run(a, b, q, 2)
+    _invariants(a, t, u, v, b, "config3")
 
 
-def test_config5_first_steps():
+# ------------------------------------------------------------------------- config 4
+def test_config4_full_cliff_spectrum():
+    n, b, q = 30000, 256, 2
+    i = np.arange(1, n + 1)
+    sig = np.where(i <= 3000, 1.0, 1e-3 * 0.999 ** (i - 3000.0))
+    a = _cm(n, n)
+    rutv.spectrum_matrix_device(a, 1, sigma=sig)  # Q1 diag(sigma) Q2' (metrics.cpp:95-110 construction)
+    t, u, v = _run(a, b, q, 2)
+    _invariants(a, t, u, v, b, "config4")
+    d = torch.diagonal(t).cpu().numpy()
+    head = np.max(np.abs(d[:3000] - 1.0))
+    rel_tail = np.abs(d[3000:] - sig[3000:]) / sig[3000:]
+    big = sig[3000:] >= 1e-9  # above the rounding floor of the generator (~ n eps ||A||_2)
+    print(f"[config4] diag head max|d-1| {head:.3e}; tail max rel {rel_tail[big].max():.4f} "
+          f"(sigma >= 1e-9, {int(big.sum())} entries), median {np.median(rel_tail[big]):.4f}")
+    assert head <= 1e-10
+    # The slowly decaying tail (0.999 per index: a b = 256 window spans a factor 0.77) is where
+    # randUTV's diagonal is only rank-revealing, not singular-value accurate.  Measured on the
+    # B200: max 0.72 (first tail window), median 0.04.  At config 2 the same comparison gives
+    # the reference's own numbers to four digits (test above), i.e. this is the algorithm's
+    # quality, not the implementation's; the reference cannot run at n = 30000 to compare.
+    assert rel_tail[big].max() <= 1.0 and np.median(rel_tail[big]) <= 0.1
+    # singular values of T against the constructed spectrum (eigenvalues of T'T on the GPU:
+    # accurate to ~ n eps sigma_1^2 / sigma, so checked where sigma >= 1e-3)
+    w = torch.linalg.eigvalsh(t.T @ t).flip(0).clamp_min(0).sqrt().cpu().numpy()
+    ok = sig >= 1e-3
+    dsv = np.max(np.abs(w[ok] - sig[ok]))
+    print(f"[config4] sigma(T) vs sigma (sigma >= 1e-3, {int(ok.sum())} values): max abs {dsv:.3e}")
+    assert dsv <= 1e-9
+
+
+# ------------------------------------------------------------------------- config 5
+def test_config5_full():
     n, b, q = 50000, 512, 2
     a = _cm(n, n)
     rutv.gaussian_matrix_device(a, 1)
-    t, u, v = _device_run(a, b, q, 2, max_steps=2)
-    nf = torch.linalg.norm(a).item()
-    # partial factorization after two steps is still an exact orthogonal equivalence
-    k = 8192  # spot-check a column slab of A = U T V'
-    res = torch.linalg.norm(a[:, :k] - u @ (t @ v[:k, :].T)).item() / torch.linalg.norm(a[:, :k]).item()
-    assert res < 1e-12, res
-    tt = t[:2 * b, :2 * b].cpu().numpy()
-    for r0 in (0, b):
-        blk = tt[r0:r0 + b, r0:r0 + b]
-        assert np.all(blk - np.diag(np.diag(blk)) == 0.0)
-        dg = np.diag(blk)
-        assert np.all(dg[:-1] >= dg[1:]) and dg[-1] >= 0
-    assert torch.all(torch.tril(t[:, :2 * b], -1) == 0.0).item()
-    assert nf > 0
+    t, u, v = _run(a, b, q, 2)
+    _invariants(a, t, u, v, b, "config5")
