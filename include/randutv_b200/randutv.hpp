@@ -161,4 +161,73 @@ inline UTVResult randutv(ConstMatrixView a, const UTVConfig& cfg) {
     return r;
 }
 
+// ---- rng.hpp:18-46: counter-based stream, deviate d a pure function of (seed, d) ----
+struct RngState {
+    std::uint64_t seed = 0;
+    std::uint64_t pos = 0;
+    explicit RngState(std::uint64_t s = 0, std::uint64_t start = 0) : seed(s), pos(start) {}
+    double normal_at(std::uint64_t d) const { return rutv_b200_normal_at(seed, d); }
+    double next_normal() { return normal_at(pos++); }
+};
+
+// ---- randutv_blocked.hpp:41-72: the public step API ----
+struct StepTransform {
+    Matrix qr;
+    std::vector<double> tau;
+    Matrix twy;
+};
+
+struct BetaFactors {
+    Matrix u;  // rt x rt, rt = min(rows(t22), bw)
+    Matrix v;  // bw x bw
+};
+
+// Right transform of one step (randutv_blocked.cpp:40-55); consumes rows(t22) * b
+// deviates of rng, drawn on the device from the same counter-based stream.
+inline StepTransform build_v_alpha(ConstMatrixView t22, idx b, int q, RngState& rng) {
+    if (b < 1) throw ConfigError("block size must be >= 1, got " + std::to_string(b));
+    if (q < 0) throw ConfigError("power iteration count must be >= 0, got " + std::to_string(q));
+    const idx rows = t22.rows, cols = t22.cols, p = cols < b ? cols : b;
+    StepTransform r;
+    r.qr = Matrix(cols, b);
+    r.tau.assign(static_cast<size_t>(p), 0.0);
+    r.twy = Matrix(p, p);
+    rutv_status st;
+    std::memset(&st, 0, sizeof st);
+    rutv_b200_build_v_alpha(0, t22.data, rows, cols, t22.ld > 0 ? t22.ld : 1, b, q, rng.seed, rng.pos, nullptr,
+                            r.qr.data(), r.tau.data(), r.twy.data(), &st);
+    detail::rethrow(st);
+    rng.pos += static_cast<std::uint64_t>(rows * b);
+    return r;
+}
+
+// Left transform of one step (randutv_blocked.cpp:57-63): the panel is factored in place.
+inline StepTransform build_u_alpha(MatrixView panel) {
+    const idx p = panel.rows < panel.cols ? panel.rows : panel.cols;
+    StepTransform r;
+    r.qr = Matrix(panel.rows, panel.cols);
+    r.tau.assign(static_cast<size_t>(p), 0.0);
+    r.twy = Matrix(p, p);
+    rutv_status st;
+    std::memset(&st, 0, sizeof st);
+    rutv_b200_build_u_alpha(0, panel.data, panel.rows, panel.cols, panel.ld > 0 ? panel.ld : 1, r.qr.data(),
+                            r.tau.data(), r.twy.data(), &st);
+    detail::rethrow(st);
+    return r;
+}
+
+// Diagonalization stage (randutv_blocked.cpp:65-81), t22 updated in place.
+inline BetaFactors beta_stage(MatrixView t22, idx bw) {
+    if (bw < 1 || bw > t22.cols)
+        throw ShapeError("beta_stage: panel width " + std::to_string(bw) + " against " + std::to_string(t22.cols) +
+                         " columns");
+    const idx rt = t22.rows < bw ? t22.rows : bw;
+    BetaFactors f{Matrix(rt, rt), Matrix(bw, bw)};
+    rutv_status st;
+    std::memset(&st, 0, sizeof st);
+    rutv_b200_beta_stage(0, t22.data, t22.rows, t22.cols, t22.ld > 0 ? t22.ld : 1, bw, f.u.data(), f.v.data(), &st);
+    detail::rethrow(st);
+    return f;
+}
+
 }  // namespace randutv

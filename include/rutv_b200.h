@@ -161,6 +161,40 @@ int rutv_b200_gaussian_matrix(int device, int64_t m, int64_t n, uint64_t seed, d
 int rutv_b200_spectrum_matrix(int device, int64_t m, int64_t n, const double* sigma, double beta,
                               uint64_t seed, double* A, int64_t lda, rutv_status* st);
 
+/* RngState(seed).normal_at(d) evaluated on the host (rng.cpp:29-36), bit-identical to
+ * the reference's stream; the drop-in header's RngState uses it. */
+double rutv_b200_normal_at(uint64_t seed, uint64_t d);
+
+/* ---------------- the reference's public step API (randutv_blocked.hpp:41-72) ----------------
+ * One step of the blocked driver, stage by stage (what the reference's own first-k-step
+ * harnesses call).  HOST-pointer entries mirror the C++ signatures; the *_device entries
+ * take DEVICE pointers and run on `stream` (0: an internal stream).  All synchronous.
+ *
+ * build_v_alpha (randutv_blocked.cpp:40-55): Y = (T22' T22)^q T22' G, G (rows x b) the
+ *   deviates pos .. pos + rows*b of RngState(seed) (or the explicit G, rows x b, ld rows),
+ *   Y = QR in place with the house() convention.  Outputs: qr (cols x b, ld cols), tau
+ *   (min(cols, b)), twy (p x p, ld p, p = min(cols, b)).  The caller advances its stream
+ *   position by rows*b, as the reference's RngState& does.
+ * build_u_alpha (randutv_blocked.cpp:57-63): the panel (rows x cols, ld) is factored in
+ *   place; qr_copy (rows x cols, ld rows; may be NULL), tau (min), twy (p x p).
+ * beta_stage (randutv_blocked.cpp:65-81): t22 (rows x cols, ld) is updated in place;
+ *   U (rt x rt, ld rt), V (bw x bw, ld bw), rt = min(rows, bw).  bw outside [1, cols] ->
+ *   RUTV_ERR_SHAPE; Jacobi sweep cap -> RUTV_ERR_CONVERGENCE. */
+int rutv_b200_build_v_alpha(int device, const double* t22, int64_t rows, int64_t cols, int64_t ld, int64_t b, int q,
+                            uint64_t seed, uint64_t pos, const double* G, double* qr, double* tau, double* twy,
+                            rutv_status* st);
+int rutv_b200_build_u_alpha(int device, double* panel, int64_t rows, int64_t cols, int64_t ld, double* qr_copy,
+                            double* tau, double* twy, rutv_status* st);
+int rutv_b200_beta_stage(int device, double* t22, int64_t rows, int64_t cols, int64_t ld, int64_t bw, double* U,
+                         double* V, rutv_status* st);
+int rutv_b200_build_v_alpha_device(int device, uint64_t stream, const double* t22, int64_t rows, int64_t cols,
+                                   int64_t ld, int64_t b, int q, uint64_t seed, uint64_t pos, const double* G,
+                                   double* qr, double* tau, double* twy, rutv_status* st);
+int rutv_b200_build_u_alpha_device(int device, uint64_t stream, double* panel, int64_t rows, int64_t cols,
+                                   int64_t ld, double* qr_copy, double* tau, double* twy, rutv_status* st);
+int rutv_b200_beta_stage_device(int device, uint64_t stream, double* t22, int64_t rows, int64_t cols, int64_t ld,
+                                int64_t bw, double* U, double* V, rutv_status* st);
+
 /* ---------------- asynchronous building blocks (distributed driver) ----------------
  * Enqueue on the calling thread's current stream (rutv_b200_set_stream; 0 =
  * legacy default stream) and return without synchronising.  DEVICE pointers.

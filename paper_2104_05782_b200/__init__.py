@@ -83,6 +83,15 @@ def lib() -> C.CDLL:
     L.rutv_b200_factorize_device.argtypes = fac
     L.rutv_b200_last_profile.argtypes = [C.POINTER(C.c_char_p), _D, C.c_int]
     L.rutv_b200_launch_count.restype = C.c_uint64
+    L.rutv_b200_normal_at.argtypes = [C.c_uint64, C.c_uint64]
+    L.rutv_b200_normal_at.restype = C.c_double
+    L.rutv_b200_build_v_alpha.argtypes = [C.c_int, C.c_void_p, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64,
+                                          C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.POINTER(Status)]
+    L.rutv_b200_build_u_alpha.argtypes = [C.c_int, C.c_void_p, _I64, _I64, _I64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.POINTER(Status)]
+    L.rutv_b200_beta_stage.argtypes = [C.c_int, C.c_void_p, _I64, _I64, _I64, _I64, C.c_void_p, C.c_void_p,
+                                       C.POINTER(Status)]
     L.rutv_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(Status)]
     L.rutv_b200_host_free.argtypes = [C.c_void_p, C.POINTER(Status)]
     L.rutv_b200_gemm_profile.argtypes = [_D, _D, C.POINTER(_I64)]
@@ -253,6 +262,67 @@ class PinnedMatrix:
             self.close()
         except Exception:
             pass
+
+
+# ---------------- the reference's public step API (randutv_blocked.hpp:41-72) ----------------
+def normal_at(seed: int, d: int) -> float:
+    """RngState(seed).normal_at(d) on the host (rng.cpp:29-36)."""
+    return float(lib().rutv_b200_normal_at(seed, d))
+
+
+def build_v_alpha(t22, b: int, q: int, seed: int, pos: int, g=None, device: int = 0):
+    """build_v_alpha (randutv_blocked.cpp:40-55) on the B200: returns (qr, tau, twy) of the
+    QR of Y = (T22' T22)^q T22' G, G = deviates pos .. pos + rows*b of RngState(seed)
+    (device-drawn) or the explicit ``g`` (rows x b, the bit-identical parity mode).  The
+    caller advances its position by rows*b, as the reference's RngState& does."""
+    t22 = np.asfortranarray(np.asarray(t22, dtype=np.float64))
+    rows, cols = t22.shape
+    p = min(cols, b)
+    qr = np.zeros((cols, b), order="F")
+    tau = np.zeros(max(p, 1))
+    twy = np.zeros((p, p), order="F")
+    gp = None
+    if g is not None:
+        g = np.asfortranarray(np.asarray(g, dtype=np.float64).reshape((rows, b), order="F"))
+        gp = _ptr(g)
+    st = Status()
+    lib().rutv_b200_build_v_alpha(device, _ptr(t22), rows, cols, max(rows, 1), b, q, seed, pos, gp, _ptr(qr),
+                                  _ptr(tau), _ptr(twy), C.byref(st))
+    _raise(st)
+    return qr, tau[:p], twy
+
+
+def build_u_alpha(panel, device: int = 0):
+    """build_u_alpha (randutv_blocked.cpp:57-63): ``panel`` (Fortran float64) is factored
+    in place; returns (qr copy, tau, twy)."""
+    if not (isinstance(panel, np.ndarray) and panel.dtype == np.float64 and panel.flags.f_contiguous):
+        raise ValueError("build_u_alpha works in place on a Fortran-ordered float64 array")
+    rows, cols = panel.shape
+    p = min(rows, cols)
+    qr = np.zeros((rows, cols), order="F")
+    tau = np.zeros(max(p, 1))
+    twy = np.zeros((p, p), order="F")
+    st = Status()
+    lib().rutv_b200_build_u_alpha(device, _ptr(panel), rows, cols, max(rows, 1), _ptr(qr), _ptr(tau), _ptr(twy),
+                                  C.byref(st))
+    _raise(st)
+    return qr, tau[:p], twy
+
+
+def beta_stage(t22, bw: int, device: int = 0):
+    """beta_stage (randutv_blocked.cpp:65-81): ``t22`` (Fortran float64) updated in place;
+    returns (u rt x rt, v bw x bw)."""
+    if not (isinstance(t22, np.ndarray) and t22.dtype == np.float64 and t22.flags.f_contiguous):
+        raise ValueError("beta_stage works in place on a Fortran-ordered float64 array")
+    rows, cols = t22.shape
+    rt = min(rows, bw)
+    u = np.zeros((max(rt, 0), max(rt, 0)), order="F")
+    v = np.zeros((max(bw, 0), max(bw, 0)), order="F")
+    st = Status()
+    lib().rutv_b200_beta_stage(device, _ptr(t22), rows, cols, max(rows, 1), bw, _ptr(u) if u.size else None,
+                               _ptr(v) if v.size else None, C.byref(st))
+    _raise(st)
+    return u, v
 
 
 def launch_count() -> int:

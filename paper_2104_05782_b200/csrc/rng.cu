@@ -11,7 +11,7 @@
 
 namespace rutv {
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z ^= z >> 30;
     z *= 0xBF58476D1CE4E5B9ULL;
     z ^= z >> 27;
@@ -20,11 +20,11 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z;
 }
 
-__device__ __forceinline__ uint64_t rng_word(uint64_t seed, uint64_t c) {
+__host__ __device__ __forceinline__ uint64_t rng_word(uint64_t seed, uint64_t c) {
     return mix64(seed + (c + 1) * 0x9E3779B97F4A7C15ULL);
 }
 
-__device__ __forceinline__ double normal_at(uint64_t seed, uint64_t d) {
+__host__ __device__ __forceinline__ double normal_at(uint64_t seed, uint64_t d) {
     const uint64_t p = d >> 1;
     const double u1 = static_cast<double>((rng_word(seed, 2 * p) >> 11) + 1) * 0x1.0p-53;
     const double u2 = static_cast<double>(rng_word(seed, 2 * p + 1) >> 11) * 0x1.0p-53;
@@ -53,3 +53,8 @@ void normal_fill(cudaStream_t stream, uint64_t seed, uint64_t pos, const DView& 
 }
 
 }  // namespace rutv
+
+// Host evaluation of the same expression (glibc log / sqrt / cos / sin, no
+// contraction): bit-identical to the reference's RngState::normal_at
+// (rng.cpp:29-36); backs the drop-in header's RngState.
+extern "C" double rutv_b200_normal_at(uint64_t seed, uint64_t d) { return rutv::normal_at(seed, d); }

@@ -231,6 +231,14 @@ size_t small_mul_scratch_bytes(size_t ndesc, int64_t total_extent);
 // dense SVDs (svd_full) with orthonormal completion; qr_prepass for m > n.
 void factorize_rect_device(cudaStream_t st, int device, int64_t m, int64_t n, const FactorArgs& fa);
 void factorize_prepass_device(cudaStream_t st, int device, int64_t m, int64_t n, const FactorArgs& fa);
+// Reference svd_full (jacobi_svd.cpp:185-192) of an m' x n' block: U m' x m', sigma
+// min(m', n'), V n' x n' (ld = their row counts); Jacobi status (4 doubles) at dev_status.
+void svd_full_device(cudaStream_t st, const DView& a, double* U, double* sigma, double* V, double* dev_status);
+// The public step API (randutv_blocked.hpp:41-72) on device views (step_api.cu).
+void build_v_alpha_device(cudaStream_t st, const DView& t22, int64_t b, int q, uint64_t seed, uint64_t pos,
+                          const double* dG, double* qr, double* tau, double* twy);
+void build_u_alpha_device(cudaStream_t st, const DView& panel, double* qr_copy, double* tau, double* twy);
+void beta_stage_device(cudaStream_t st, const DView& t22, int64_t bw, double* U, double* V, double* dev_status);
 // X <- Q X with Q = H_1...H_p from packed qr (householder.cpp:116-127, blocked).
 void apply_q_left_blocked(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
                           double* scratch, int64_t scratch_elems);

@@ -2,6 +2,7 @@
 // Mirrors the reference's own usage (tests/test_randutv_blocked.cpp:40-78):
 // factor, then check ||A - U T V'||_F / ||A||_F and U'U = I.
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 
 #include "randutv_b200/randutv.hpp"
@@ -49,6 +50,32 @@ int main() {
     } catch (const randutv::ConfigError&) {
         err_ok = true;
     }
-    std::printf("shim: resid=%.3e orth=%.3e config_error=%d\n", resid, od, err_ok ? 1 : 0);
-    return (resid < 1e-13 && od < 1e-12 && err_ok) ? 0 : 1;
+    // the public step API (randutv_blocked.hpp:41-72): one step by hand
+    randutv::RngState rng(cfg.seed);
+    randutv::StepTransform sv = randutv::build_v_alpha(a.view(), cfg.b, cfg.q, rng);
+    bool step_ok = rng.pos == static_cast<std::uint64_t>(n * cfg.b) && sv.qr.rows() == n &&
+                   sv.qr.cols() == cfg.b && sv.twy.rows() == cfg.b && sv.tau.size() == static_cast<size_t>(cfg.b);
+    randutv::Matrix panel(n, cfg.b);
+    for (randutv::idx j = 0; j < cfg.b; ++j)
+        for (randutv::idx i = 0; i < n; ++i) panel(i, j) = a(i, j);
+    randutv::StepTransform su = randutv::build_u_alpha(panel.view());
+    for (randutv::idx j = 0; j < cfg.b; ++j) step_ok = step_ok && su.qr(j, j) == panel(j, j) && panel(j, j) >= 0.0;
+    randutv::Matrix t22(n, n);
+    for (randutv::idx j = 0; j < n; ++j)
+        for (randutv::idx i = 0; i < n; ++i) t22(i, j) = (j < cfg.b) ? (i <= j ? panel(i, j) : 0.0) : a(i, j);
+    randutv::BetaFactors bf = randutv::beta_stage(t22.view(), cfg.b);
+    for (randutv::idx j = 0; j < cfg.b; ++j)
+        for (randutv::idx i = 0; i < n; ++i)
+            step_ok = step_ok && (i == j ? (t22(i, j) >= 0.0 && (j == 0 || t22(j - 1, j - 1) >= t22(i, j)))
+                                         : t22(i, j) == 0.0);
+    step_ok = step_ok && bf.u.rows() == cfg.b && bf.v.rows() == cfg.b;
+    bool shape_err = false;
+    try {
+        randutv::beta_stage(t22.view(), n + 1);
+    } catch (const randutv::ShapeError&) {
+        shape_err = true;
+    }
+    std::printf("shim: resid=%.3e orth=%.3e config_error=%d step_api=%d shape_error=%d\n", resid, od,
+                err_ok ? 1 : 0, step_ok ? 1 : 0, shape_err ? 1 : 0);
+    return (resid < 1e-13 && od < 1e-12 && err_ok && step_ok && shape_err) ? 0 : 1;
 }
