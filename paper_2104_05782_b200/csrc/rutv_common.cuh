@@ -33,10 +33,12 @@ struct Error : std::runtime_error {
 #define RUTV_CUDA(x)                                                                  \
     do {                                                                              \
         cudaError_t e_ = (x);                                                         \
-        if (e_ != cudaSuccess)                                                        \
+        if (e_ != cudaSuccess) {                                                      \
+            cudaGetLastError(); /* a failed API call must not poison the next launch check */ \
             throw ::rutv::Error(RUTV_ERR_CUDA, std::string("CUDA error ") +           \
                                                    cudaGetErrorString(e_) + " at " +  \
                                                    __FILE__ + ":" + std::to_string(__LINE__)); \
+        }                                                                             \
     } while (0)
 
 #define RUTV_CHECK_LAUNCH() RUTV_CUDA(cudaGetLastError())

@@ -224,7 +224,7 @@ int rutv_b200_build_v_alpha(int device, const double* t22, int64_t rows, int64_t
             rutv::build_v_alpha_device(cs.s, DView(rows, cols, std::max<int64_t>(rows, 1), dT.p), b, q, seed, pos,
                                        G ? dG.p : nullptr, dQ.p, dtau.p, dtw.p);
             d2h(qr, std::max<int64_t>(cols, 1), dQ.p, std::max<int64_t>(cols, 1), cols, b, cs.s);
-            d2h(tau, 1, dtau.p, 1, p, 1, cs.s);
+            d2h(tau, std::max<int64_t>(p, 1), dtau.p, std::max<int64_t>(p, 1), p, 1, cs.s);
             d2h(twy, std::max<int64_t>(p, 1), dtw.p, std::max<int64_t>(p, 1), p, p, cs.s);
             RUTV_CUDA(cudaStreamSynchronize(cs.s));
         }
@@ -244,7 +244,7 @@ int rutv_b200_build_u_alpha(int device, double* panel, int64_t rows, int64_t col
             rutv::build_u_alpha_device(cs.s, DView(rows, cols, l, dP.p), nullptr, dtau.p, dtw.p);
             d2h(panel, ld, dP.p, l, rows, cols, cs.s);
             d2h(qr_copy, l, dP.p, l, rows, cols, cs.s);
-            d2h(tau, 1, dtau.p, 1, p, 1, cs.s);
+            d2h(tau, std::max<int64_t>(p, 1), dtau.p, std::max<int64_t>(p, 1), p, 1, cs.s);
             d2h(twy, std::max<int64_t>(p, 1), dtw.p, std::max<int64_t>(p, 1), p, p, cs.s);
             RUTV_CUDA(cudaStreamSynchronize(cs.s));
         }

@@ -37,6 +37,8 @@ def test_sanitizer_clean(tool, mode):
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1200)
     text = out.stdout + out.stderr
+    if "closed on this pool" in text:  # the GPU pool's wrapper refuses compute-sanitizer
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + text.strip().splitlines()[0][:200])
     assert out.returncode == 0, text[-4000:]
     assert "sanitize case ok" in text
     assert "ERROR SUMMARY: 0 errors" in text, text[-4000:]

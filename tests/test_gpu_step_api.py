@@ -54,7 +54,12 @@ def test_step_api_replay_matches_oracle(n, b, q, steps):
     a = oracle.gaussian_matrix(n, n, 1000 + n)
     got = _replay(a, b, q, 9, steps)
     ref = oracle.randutv(a, b=b, q=q, seed=9, max_steps=steps)
-    compare_to_oracle(a, got, ref, t_tol=1e-12, uv_tol=1e-10, diag_rel=1e-10)
+    # the unfinished trailing block's diagonal is raw (not yet SVD'd) and may be tiny: the
+    # pure-relative diag test applies to the finished windows
+    compare_to_oracle(a, got, ref, t_tol=1e-12, uv_tol=1e-10, diag_rel=1e-6)
+    k = min(steps * b, n)
+    dg, dr = np.diag(got[0])[:k], np.diag(ref[0])[:k]
+    assert np.max(np.abs(dg - dr) / np.abs(dr)) <= 1e-10
 
 
 def test_build_v_alpha_device_rng_and_position():
