@@ -62,8 +62,14 @@ typedef struct {
     int32_t overlap;    /* 1: off-critical-path updates on a second stream  */
     int32_t reserved0;
     uint64_t stream;    /* cudaStream_t to run on (0: an internal stream)    */
-    int32_t reserved[4];
+    int32_t grid_p;     /* 2D block-cyclic process grid (block_cyclic.cpp:26-38): grid_p x grid_q  */
+    int32_t grid_q;     /* GPUs; 1 x 1 = one GPU.  Host-pointer rutv_b200_factorize only (square). */
+    int32_t grid_sim;   /* 1: run the grid's ranks as threads on o->device with an in-process      */
+                        /*    exchange instead of NCCL (validation of the sharded path on 1 GPU)   */
+    int32_t reserved1;
 } rutv_opts;
+
+#define RUTV_NCCL_ID_BYTES 128
 
 /* Fills the reference defaults: b=128, q=1, build_u=build_v=1, seed=0,
  * device=0, max_steps=-1, overlap=1. */
@@ -160,6 +166,37 @@ int rutv_b200_gaussian_matrix(int device, int64_t m, int64_t n, uint64_t seed, d
  * s *= beta as metrics.cpp:103-106 does).  A: DEVICE pointer. */
 int rutv_b200_spectrum_matrix(int device, int64_t m, int64_t n, const double* sigma, double beta,
                               uint64_t seed, double* A, int64_t lda, rutv_status* st);
+
+/* ---------------- sharded factorization on a P x Q grid of GPUs ----------------
+ * The reference's distributed randUTV is ScaLAPACK over MPI on the 2D
+ * block-cyclic layout of block_cyclic.cpp:26-38.  Here: one rank per GPU, T/U/V distributed
+ * identically in b x b blocks, block (br, bc) on rank (br mod P)*Q + (bc mod Q), stored at
+ * local block (br div P, bc div Q); collectives over NCCL (NVLink).
+ *
+ * Single process, host buffers: rutv_b200_factorize with o->grid_p * o->grid_q > 1 (one host
+ * thread per GPU, devices 0 .. P*Q-1, an NCCL clique) -- the C++ drop-in's
+ * UTVConfig{grid_p, grid_q} path.
+ * One process per GPU (torchrun / MPI launchers): rank 0 makes an id with
+ * rutv_b200_nccl_unique_id, ships it to every rank out of band, every rank calls
+ * rutv_b200_dist_create and then rutv_b200_factorize_dist on its local blocks (DEVICE
+ * pointers; local shape from rutv_b200_grid_local_shape).  Collective calls: every rank of
+ * the grid must make them, in the same order. */
+typedef struct rutv_dist_ctx rutv_dist_ctx;
+int rutv_b200_grid_local_shape(int64_t n, int64_t b, int P, int Q, int rank, int64_t* rows, int64_t* cols);
+/* full (n x n, ldf) <-> rank's local blocks (ldl); any memory kinds (cudaMemcpyDefault). */
+int rutv_b200_grid_copy(int device, int64_t n, int64_t b, int P, int Q, int rank, double* full, int64_t ldf,
+                        double* loc, int64_t ldl, int to_local, rutv_status* st);
+int rutv_b200_nccl_unique_id(unsigned char* id, rutv_status* st);
+int rutv_b200_dist_create(const unsigned char* id, int P, int Q, int rank, int device, rutv_dist_ctx** out,
+                          rutv_status* st);
+int rutv_b200_dist_destroy(rutv_dist_ctx* ctx, rutv_status* st);
+/* A_loc (local rows x local cols) is read; T_loc / U_loc / V_loc written (in place, no copies,
+ * when V_loc sits directly on top of T_loc: T_loc == V_loc + local rows, ldt == ldv).  G: the
+ * full explicit stream on this device (parity mode) or NULL (device RNG, each rank draws its
+ * own rows).  o->stream, o->overlap, o->max_steps honoured. */
+int rutv_b200_factorize_dist(rutv_dist_ctx* ctx, const rutv_opts* o, int64_t n, const double* A_loc, int64_t lda,
+                             const double* G, int64_t g_len, double* T_loc, int64_t ldt, double* U_loc, int64_t ldu,
+                             double* V_loc, int64_t ldv, rutv_status* st);
 
 /* RngState(seed).normal_at(d) evaluated on the host (rng.cpp:29-36), bit-identical to
  * the reference's stream; the drop-in header's RngState uses it. */

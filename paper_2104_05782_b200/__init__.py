@@ -53,7 +53,8 @@ class Opts(C.Structure):
     _fields_ = [("b", C.c_int64), ("q", C.c_int32), ("build_u", C.c_int32), ("build_v", C.c_int32),
                 ("qr_prepass", C.c_int32), ("seed", C.c_uint64), ("device", C.c_int32),
                 ("max_steps", C.c_int32), ("overlap", C.c_int32), ("reserved0", C.c_int32),
-                ("stream", C.c_uint64), ("reserved", C.c_int32 * 4)]
+                ("stream", C.c_uint64), ("grid_p", C.c_int32), ("grid_q", C.c_int32),
+                ("grid_sim", C.c_int32), ("reserved1", C.c_int32)]
 
 
 _D = C.POINTER(C.c_double)
@@ -92,6 +93,16 @@ def lib() -> C.CDLL:
                                           C.c_void_p, C.POINTER(Status)]
     L.rutv_b200_beta_stage.argtypes = [C.c_int, C.c_void_p, _I64, _I64, _I64, _I64, C.c_void_p, C.c_void_p,
                                        C.POINTER(Status)]
+    # sharded path (dist.cu)
+    L.rutv_b200_grid_local_shape.argtypes = [_I64, _I64, C.c_int, C.c_int, C.c_int, C.POINTER(_I64), C.POINTER(_I64)]
+    L.rutv_b200_grid_copy.argtypes = [C.c_int, _I64, _I64, C.c_int, C.c_int, C.c_int, C.c_void_p, _I64, C.c_void_p,
+                                      _I64, C.c_int, C.POINTER(Status)]
+    L.rutv_b200_nccl_unique_id.argtypes = [C.c_void_p, C.POINTER(Status)]
+    L.rutv_b200_dist_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                        C.POINTER(Status)]
+    L.rutv_b200_dist_destroy.argtypes = [C.c_void_p, C.POINTER(Status)]
+    L.rutv_b200_factorize_dist.argtypes = [C.c_void_p, C.POINTER(Opts), _I64, C.c_void_p, _I64, C.c_void_p, _I64,
+                                           C.c_void_p, _I64, C.c_void_p, _I64, C.c_void_p, _I64, C.POINTER(Status)]
     L.rutv_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(Status)]
     L.rutv_b200_host_free.argtypes = [C.c_void_p, C.POINTER(Status)]
     L.rutv_b200_gemm_profile.argtypes = [_D, _D, C.POINTER(_I64)]
@@ -154,9 +165,11 @@ def _raise(st: Status) -> None:
 
 def make_opts(b: int = 128, q: int = 1, seed: int = 0, build_u: bool = True, build_v: bool = True,
               qr_prepass: bool = False, device: int = 0, max_steps: int = -1,
-              overlap: bool = True, stream: int = 0) -> Opts:
+              overlap: bool = True, stream: int = 0, grid=(1, 1), grid_sim: bool = False) -> Opts:
     o = Opts()
     lib().rutv_b200_default_opts(C.byref(o))
+    o.grid_p, o.grid_q = int(grid[0]), int(grid[1])
+    o.grid_sim = int(grid_sim)
     o.b, o.q, o.seed = int(b), int(q), int(seed)
     o.build_u, o.build_v, o.qr_prepass = int(build_u), int(build_v), int(qr_prepass)
     o.device, o.max_steps, o.overlap = int(device), int(max_steps), int(overlap)
@@ -180,12 +193,14 @@ def _ptr(x: np.ndarray):
 
 def factorize(a, *, b: int = 0, q: int = 1, algo: str = "b200", seed: int = 0,
               build_uv: bool = True, qr_prepass: bool = False, g=None, device: int = 0,
-              max_steps: int = -1):
+              max_steps: int = -1, grid=(1, 1), grid_sim: bool = False):
     """Factor ``a`` as ``u @ t @ v.T`` on the B200 (bindings.cpp:49-66 semantics).
 
     ``g``: optional 1-D array with the first ``stream_length(m, n, b)`` deviates
     of ``RngState(seed)`` -- the bit-identical parity mode; otherwise the sketch
     is drawn on the device from the same counter-based stream.
+    ``grid=(P, Q)``: shard over a P x Q block-cyclic grid of GPUs (devices 0 .. P*Q-1, NCCL);
+    ``grid_sim=True`` runs the grid's ranks as threads on ``device`` instead (validation).
     Returns ``(t, u, v)``; ``u``/``v`` are None when ``build_uv`` is False."""
     if algo != "b200":
         raise ValueError(f"algo must be 'b200' on this build, got '{algo}'")
@@ -195,7 +210,7 @@ def factorize(a, *, b: int = 0, q: int = 1, algo: str = "b200", seed: int = 0,
     m, n = a.shape
     bb = b if b > 0 else 128
     o = make_opts(b=bb, q=q, seed=seed, build_u=build_uv, build_v=build_uv,
-                  qr_prepass=qr_prepass, device=device, max_steps=max_steps)
+                  qr_prepass=qr_prepass, device=device, max_steps=max_steps, grid=grid, grid_sim=grid_sim)
     t = np.zeros((m, n), order="F")
     u = np.zeros((m, m), order="F") if build_uv else None
     v = np.zeros((n, n), order="F") if build_uv else None
@@ -323,6 +338,76 @@ def beta_stage(t22, bw: int, device: int = 0):
                                _ptr(v) if v.size else None, C.byref(st))
     _raise(st)
     return u, v
+
+
+# ---------------- sharded path: one process per GPU (dist.cu) ----------------
+def grid_local_shape(n: int, b: int, P: int, Q: int, rank: int) -> tuple[int, int]:
+    """(local rows, local cols) of ``rank`` on the P x Q block-cyclic grid (block_cyclic.cpp:26-38)."""
+    r, c = _I64(0), _I64(0)
+    if lib().rutv_b200_grid_local_shape(n, b, P, Q, rank, C.byref(r), C.byref(c)) != RUTV_OK:
+        raise ValueError("bad grid")
+    return r.value, c.value
+
+
+def grid_copy(full, loc, n: int, b: int, P: int, Q: int, rank: int, to_local: bool) -> None:
+    """Full n x n column-major CUDA tensor <-> this rank's local blocks (column-major CUDA tensor)."""
+    pf, _, _, ldf = _cm(full)
+    pl, _, _, ldl = _cm(loc)
+    st = Status()
+    lib().rutv_b200_grid_copy(loc.device.index or 0, n, b, P, Q, rank, pf, ldf, pl, ldl, int(to_local), C.byref(st))
+    _raise(st)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    st = Status()
+    lib().rutv_b200_nccl_unique_id(buf, C.byref(st))
+    _raise(st)
+    return bytes(buf)
+
+
+class DistContext:
+    """One rank of a P x Q grid (its NCCL communicators); collective to create."""
+
+    def __init__(self, uid: bytes, P: int, Q: int, rank: int, device: int):
+        self.P, self.Q, self.rank, self.device = P, Q, rank, device
+        self.h = C.c_void_p()
+        idb = (C.c_ubyte * 128).from_buffer_copy(uid)
+        st = Status()
+        lib().rutv_b200_dist_create(idb, P, Q, rank, device, C.byref(self.h), C.byref(st))
+        _raise(st)
+
+    def close(self) -> None:
+        if self.h is not None and self.h.value:
+            st = Status()
+            lib().rutv_b200_dist_destroy(self.h, C.byref(st))
+            self.h = None
+
+    def factorize(self, n: int, a_loc, t_loc, u_loc=None, v_loc=None, *, b: int = 128, q: int = 1, seed: int = 0,
+                  g=None, stream: int = 0, max_steps: int = -1, overlap: bool = True) -> None:
+        """This rank's part of the sharded factorization (column-major CUDA tensors: A, T, U, V
+        local blocks; in place when v_loc sits directly on top of t_loc in one buffer)."""
+        def info(x):
+            if x is None:
+                return None, 1
+            return C.c_void_p(x.data_ptr()), max(x.stride(1) if x.shape[1] > 1 else x.shape[0], x.shape[0], 1)
+        o = make_opts(b=b, q=q, seed=seed, build_u=u_loc is not None, build_v=v_loc is not None,
+                      device=self.device, max_steps=max_steps, overlap=overlap, stream=stream)
+        pa, lda = info(a_loc)
+        pt, ldt = info(t_loc)
+        pu, ldu = info(u_loc)
+        pv, ldv = info(v_loc)
+        gp, glen = (C.c_void_p(g.data_ptr()), g.numel()) if g is not None else (None, 0)
+        st = Status()
+        lib().rutv_b200_factorize_dist(self.h, C.byref(o), n, pa, lda, gp, glen, pt, ldt, pu, ldu, pv, ldv,
+                                       C.byref(st))
+        _raise(st)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def launch_count() -> int:

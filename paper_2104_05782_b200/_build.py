@@ -24,7 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
 # The device RNG restates the reference's no-contraction arithmetic
 # (proj/CMakeLists.txt:17-18 -ffp-contract=off) -> no FMA fusion there.
 PER_FILE = {"rng.cu": ["--fmad=false"]}
-SOURCES = ["gemm_f64.cu", "rng.cu", "aux_kernels.cu", "qr_cluster.cu", "qr_reg.cu", "cholqr.cu", "jacobi.cu", "randutv.cu", "rect.cu", "grouped.cu", "gen.cu", "capi.cu", "stream_api.cu", "io_metrics.cu", "runtime.cu", "step_api.cu"]
+SOURCES = ["gemm_f64.cu", "rng.cu", "aux_kernels.cu", "qr_cluster.cu", "qr_reg.cu", "cholqr.cu", "jacobi.cu", "randutv.cu", "rect.cu", "grouped.cu", "gen.cu", "capi.cu", "stream_api.cu", "io_metrics.cu", "runtime.cu", "step_api.cu", "dist.cu"]
 
 
 def _digest() -> str:
@@ -66,7 +66,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
+    # NCCL is dlopen'ed at first use by the sharded path (dist.cu), not linked: an
+    # already-loaded libnccl.so.2 (torch's) must win over the system one
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"], check=True)
     os.replace(tmp, LIB)
     with open(LIB + ".sha256", "w") as f:
         f.write(_digest())

@@ -147,6 +147,8 @@ void rutv_b200_default_opts(rutv_opts* o) {
     o->device = 0;
     o->max_steps = -1;
     o->overlap = 1;
+    o->grid_p = 1;
+    o->grid_q = 1;
 }
 
 int64_t rutv_b200_stream_length(int64_t m, int64_t n, int64_t b) {
@@ -194,6 +196,15 @@ int rutv_b200_factorize(const rutv_opts* o, const double* A, int64_t m, int64_t 
         const bool prepass = o->qr_prepass && m > n;  // the inner n x n run draws the stream
         const int64_t glen = G ? drawn_length(prepass ? n : m, n, o->b, o->max_steps) : 0;
         if (G && glen > 0 && g_len < glen) throw Error(RUTV_ERR_SHAPE, "explicit G shorter than the stream");
+        if (std::max(o->grid_p, 1) * std::max(o->grid_q, 1) > 1) {  // sharded over a P x Q grid (dist.cu)
+            if (m != n || prepass) throw Error(RUTV_ERR_NOTIMPL, "the sharded path factors square matrices");
+            if (o->build_u && (!U || ldu < std::max<int64_t>(m, 1))) throw Error(RUTV_ERR_SHAPE, "U buffer");
+            if (o->build_v && (!V || ldv < std::max<int64_t>(n, 1))) throw Error(RUTV_ERR_SHAPE, "V buffer");
+            if (lda < std::max<int64_t>(m, 1) || ldt < std::max<int64_t>(m, 1))
+                throw Error(RUTV_ERR_SHAPE, "leading dimension smaller than the row count");
+            rutv::factorize_grid_host(o, A, n, lda, G, glen, T, ldt, U, ldu, V, ldv);
+            return;
+        }
         auto h2d = [&](double* d, int64_t ldd, const double* h, int64_t ldh, int64_t r, int64_t c) {
             if (r * c > 0)
                 RUTV_CUDA(cudaMemcpy2DAsync(d, static_cast<size_t>(ldd) * 8, h, static_cast<size_t>(ldh) * 8,

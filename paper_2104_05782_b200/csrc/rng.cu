@@ -52,6 +52,32 @@ void normal_fill(cudaStream_t stream, uint64_t seed, uint64_t pos, const DView& 
     RUTV_CHECK_LAUNCH();
 }
 
+// Block-cyclic rows of a step's G (s x cols, column-major in the stream):
+// out(lr, j) = G((first + (lr / b) * stride) * b + lr % b, j), i.e. deviate
+// pos + that row + j * s -- a rank's own rows of the replicated sketch matrix,
+// drawn without communication (the stream is counter-based, rng.hpp:9-17).
+__global__ void normal_fill_cyclic_kernel(uint64_t seed, uint64_t pos, int64_t s, int64_t b, int64_t first,
+                                          int64_t stride, int64_t rows, int64_t cols, double* g, int64_t ld) {
+    const int64_t total = rows * cols;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i % rows, c = i / rows;
+        const int64_t gr = (first + (r / b) * stride) * b + r % b;
+        g[r + c * ld] = normal_at(seed, pos + static_cast<uint64_t>(gr + c * s));
+    }
+}
+
+void normal_fill_cyclic(cudaStream_t stream, uint64_t seed, uint64_t pos, int64_t s, int64_t b, int64_t first,
+                        int64_t stride, const DView& g) {
+    const int64_t total = g.rows * g.cols;
+    if (total == 0) return;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
+    normal_fill_cyclic_kernel<<<blocks, 256, 0, stream>>>(seed, pos, s, b, first, stride, g.rows, g.cols, g.data,
+                                                          g.ld);
+    note_launch();
+    RUTV_CHECK_LAUNCH();
+}
+
 }  // namespace rutv
 
 // Host evaluation of the same expression (glibc log / sqrt / cos / sin, no

@@ -117,6 +117,14 @@ int gemm_profile_get(double* flops, double* ms, int64_t* launches);
 
 // G(i, j) = normal_at(seed, pos + i + j*rows)  (proj/src/rng.cpp:29-53).
 void normal_fill(cudaStream_t stream, uint64_t seed, uint64_t pos, const DView& g);
+// A rank's block-cyclic rows of a step's G (s x cols): g(lr, j) = G((first + (lr/b)*stride)*b
+// + lr%b, j) with G(i, j) = normal_at(seed, pos + i + j*s) (rng.cu).
+void normal_fill_cyclic(cudaStream_t stream, uint64_t seed, uint64_t pos, int64_t s, int64_t b, int64_t first,
+                        int64_t stride, const DView& g);
+// small rows [t*b, t*b + w_t) <-> big rows [(first + t*stride)*b, ...), t < count; scatter writes
+// big (stream_api.cu) -- row-block gather / scatter of block-cyclic layouts.
+void block_rows(cudaStream_t st, double* small, int64_t lds_small, double* big, int64_t ld_big, int64_t big_rows,
+                int64_t cols, int64_t b, int64_t first, int64_t stride, int64_t count, bool scatter);
 
 // Small elementwise kernels.
 void set_identity(cudaStream_t stream, const DView& a);
@@ -241,6 +249,9 @@ void build_v_alpha_device(cudaStream_t st, const DView& t22, int64_t b, int q, u
                           const double* dG, double* qr, double* tau, double* twy);
 void build_u_alpha_device(cudaStream_t st, const DView& panel, double* qr_copy, double* tau, double* twy);
 void beta_stage_device(cudaStream_t st, const DView& t22, int64_t bw, double* U, double* V, double* dev_status);
+// The sharded driver over a P x Q grid from HOST buffers (dist.cu; one thread per rank).
+void factorize_grid_host(const rutv_opts* o, const double* A, int64_t n, int64_t lda, const double* G, int64_t glen,
+                         double* T, int64_t ldt, double* U, int64_t ldu, double* V, int64_t ldv);
 // X <- Q X with Q = H_1...H_p from packed qr (householder.cpp:116-127, blocked).
 void apply_q_left_blocked(cudaStream_t st, const DView& qr, const double* tau, int64_t p, const DView& x,
                           double* scratch, int64_t scratch_elems);

@@ -48,7 +48,7 @@ struct Scratch {
     cudaStream_t s;
     Scratch(int64_t elems, cudaStream_t st) : s(st) {
         if (elems < 1) elems = 1;
-        RUTV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), static_cast<size_t>(elems) * 8, st));
+        p = static_cast<double*>(rutv::dev_alloc(static_cast<size_t>(elems) * 8, st));
     }
     ~Scratch() {
         if (p) cudaFreeAsync(p, s);
@@ -76,6 +76,19 @@ __global__ void block_rows_kernel(double* dst, int64_t ldd, const double* src, i
 }
 
 }  // namespace
+
+namespace rutv {
+void block_rows(cudaStream_t st, double* small, int64_t lds_small, double* big, int64_t ld_big, int64_t big_rows,
+                int64_t cols, int64_t b, int64_t first, int64_t stride, int64_t count, bool scatter) {
+    const int64_t total = count * b * cols;
+    if (total <= 0) return;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
+    block_rows_kernel<<<blocks, 256, 0, st>>>(small, lds_small, big, ld_big, cols, b, first, stride, count, big_rows,
+                                              scatter ? 1 : 0);
+    note_launch();
+    RUTV_CHECK_LAUNCH();
+}
+}  // namespace rutv
 
 extern "C" {
 
