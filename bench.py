@@ -324,7 +324,8 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one independent factorization per GPU (weak scaling) instead of the sharded "
                          "2D block-cyclic factorization of one matrix")
-    ap.add_argument("--sharded", action="store_true", help="(default for N > 1; kept for compatibility)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="the sharded driver even at N = 1 (a 1 x 1 NCCL grid; default for N > 1)")
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="timed host-pointer steps (default: K, or 2 when n >= 20000)")
     ap.add_argument("--profile-steps", type=int, default=None,
@@ -358,8 +359,8 @@ def main():
     dev = torch.device(f"cuda:{local}")
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        if not args.replicas:
-            return run_sharded(args, torch, dist, rutv, world, rank, local, dev, args.flops)
+    if (world > 1 and not args.replicas) or args.sharded:
+        return run_sharded(args, torch, dist, rutv, world, rank, local, dev, args.flops)
     n, b, q, F = args.n, args.b, args.q, args.flops
     assert abs(F - rutv.flops(n, b, q)) <= 1e-9 * F
 
@@ -529,26 +530,36 @@ def flops(n, b, q):
 
 # ---------------------------------------------------------- sharded (2D) --
 def run_sharded(args, torch, dist, rutv, world, rank, local, dev, F):
-    """ONE matrix on the P x Q block-cyclic grid (dist.py): strong scaling.
+    """ONE matrix on the P x Q block-cyclic grid: the C++ sharded driver (dist.cu,
+    rutv_b200_factorize_dist) over NCCL, one rank per GPU -- strong scaling.
     value = F / (max over ranks of the device time of one factorization)."""
-    from paper_2104_05782_b200.dist import CudaOps, Grid, factorize_dist, grid_shape, make_comms, scatter_grid
+    from paper_2104_05782_b200.dist import grid_shape
     n, b, q = args.n, args.b, args.q
     P, Q = grid_shape(world)
-    grid = Grid(n, b, P, Q, rank)
-    comms = make_comms(grid) if world > 1 else None
+    uid = [rutv.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    ctx = rutv.DistContext(uid[0], P, Q, rank, local)
+    log(f"[bench] rank {rank}: NCCL grid {P}x{Q} communicators up on cuda:{local}")
+    mr, mc = rutv.grid_local_shape(n, b, P, Q, rank)
     full = cm(torch, n, n, dev)
     make_matrix(rutv, full, args.kind, SEED_A)  # same matrix on every rank (deterministic generator)
-    a_loc = scatter_grid(full, grid)
+    a_loc = cm(torch, mr, mc, dev)
+    rutv.grid_copy(full, a_loc, n, b, P, Q, rank, to_local=True)
     del full
+    torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    ops = CudaOps(dev)
+    vt = cm(torch, 2 * mr, mc, dev)  # [V; T] stacked: factored in place
+    t_loc, v_loc = vt[mr:, :], vt[:mr, :]
+    u_loc = cm(torch, mr, mc, dev)
     stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
 
-    def step(x):
-        return factorize_dist(x, grid, q=q, seed=SEED_G, ops=ops, comms=comms)
+    def step(a_src=None):
+        ctx.factorize(n, a_loc if a_src is None else a_src, t_loc, u_loc, v_loc, b=b, q=q, seed=SEED_G, stream=sh)
 
     for _ in range(args.warmup):
-        step(a_loc)
+        step()
     torch.cuda.synchronize()
     launches0 = rutv.launch_count()
     with ClockSampler(local) as clk:
@@ -558,7 +569,7 @@ def run_sharded(args, torch, dist, rutv, world, rank, local, dev, F):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            step(a_loc)
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -568,32 +579,35 @@ def run_sharded(args, torch, dist, rutv, world, rank, local, dev, F):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    # e2e: this rank's blocks from pinned host memory, results back to pinned host memory
+    # e2e: this rank's blocks from pinned host memory, its T, U, V blocks back to pinned host memory
     e2e = None
     if not args.no_e2e:
-        mr, mc = a_loc.shape
-        ha = torch.empty((mc, mr), dtype=torch.float64, pin_memory=True).T
-        ha.copy_(a_loc)
-        hout = [torch.empty((mc, mr), dtype=torch.float64, pin_memory=True).T for _ in range(3)]
-        dbuf = torch.empty_like(a_loc)
+        ha = rutv.PinnedMatrix(mr, mc)
+        rutv.copy_matrix_async(ha.array, a_loc, sh)
+        hout = [rutv.PinnedMatrix(mr, mc) for _ in range(3)]
+        dbuf = cm(torch, mr, mc, dev)
+        steps_e = args.e2e_steps
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(args.steps):
-            dbuf.copy_(ha, non_blocking=True)
-            t, u, v = step(dbuf)
-            for h, d in zip(hout, (t, u, v)):
-                h.copy_(d, non_blocking=True)
+        for _ in range(steps_e):
+            rutv.copy_matrix_async(dbuf, ha.array, sh)  # pinned host -> HBM on the timed stream
+            step(dbuf)
+            for h, d in zip(hout, (t_loc, u_loc, v_loc)):
+                rutv.copy_matrix_async(h.array, d, sh)
         f1.record(stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
+        ems = torch.tensor([f0.elapsed_time(f1) / steps_e], device=dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": round(F / (float(ems.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
-               "ms_per_step": round(float(ems.item()), 3),
+               "ms_per_step": round(float(ems.item()), 3), "steps": steps_e,
                "h2d_bytes_per_step": 8 * mr * mc, "d2h_bytes_per_step": 3 * 8 * mr * mc, "per_rank": True}
+        for h in [ha, *hout]:
+            h.close()
+    ctx.close()
     if rank == 0:
         value = F / (ms / 1e3) / 1e9
         line = {
@@ -601,13 +615,12 @@ def run_sharded(args, torch, dist, rutv, world, rank, local, dev, F):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (device-generated {KIND_TEXT[args.kind]}, seed {SEED_A})",
-            "config": {"workload": workload_name(n, b, q, args.kind, args.config), "n": n, "b": b, "q": q,
-                       "flops_per_step": F, "parallelism": f"2d-block-cyclic {P}x{Q}",
-                       "l2": "state exceeds the 126 MB L2; no flush"},
+            "config": config_dict(args, f"2d-block-cyclic {P}x{Q}"),
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "roofline": {"bound": "tensor", "achieved": round(value / 1e3 / world, 3), "peak": DMMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(value / 1e3 / world / DMMA_PEAK_TFLOPS, 4),
-                         "traffic": None, "kernel": "whole factorization per GPU (dist driver)"},
+                         "traffic": None, "kernel": "whole sharded factorization per GPU (dist.cu)",
+                         "step_frac_of_peak": round(value / 1e3 / world / DMMA_PEAK_TFLOPS, 4)},
             "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)

@@ -116,6 +116,11 @@ uint64_t rutv_b200_launch_count(void);
  * the host-pointer entry points copy at full PCIe/C2C bandwidth from them. */
 int rutv_b200_host_alloc(size_t bytes, void** p, rutv_status* st);
 int rutv_b200_host_free(void* p, rutv_status* st);
+/* Asynchronous column-major copy of a rows x cols FP64 matrix between any two memory kinds
+ * (cudaMemcpy2DAsync, cudaMemcpyDefault) on `stream` (the staging step of host-pointer
+ * callers of the DEVICE-pointer entry points, e.g. rutv_b200_factorize_dist). */
+int rutv_b200_copy_matrix_async(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                                int64_t cols, uint64_t stream, rutv_status* st);
 
 /* GEMM-kernel totals of the last factorize call on this thread when
  * RUTV_GEMM_PROFILE=1 (CUDA events around every GEMM launch): algorithmic

@@ -105,6 +105,8 @@ def lib() -> C.CDLL:
                                            C.c_void_p, _I64, C.c_void_p, _I64, C.c_void_p, _I64, C.POINTER(Status)]
     L.rutv_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(Status)]
     L.rutv_b200_host_free.argtypes = [C.c_void_p, C.POINTER(Status)]
+    L.rutv_b200_copy_matrix_async.argtypes = [C.c_void_p, _I64, C.c_void_p, _I64, _I64, _I64, C.c_uint64,
+                                              C.POINTER(Status)]
     L.rutv_b200_gemm_profile.argtypes = [_D, _D, C.POINTER(_I64)]
     L.rutv_b200_gaussian_matrix.argtypes = [C.c_int, _I64, _I64, C.c_uint64, C.c_void_p, _I64,
                                             C.POINTER(Status)]
@@ -408,6 +410,29 @@ class DistContext:
             self.close()
         except Exception:
             pass
+
+
+def _mat_ptr(x):
+    """(pointer, rows, cols, ld) of a column-major FP64 matrix: a Fortran-ordered numpy array
+    (e.g. PinnedMatrix.array) or a column-major torch tensor (stride (1, ld))."""
+    if isinstance(x, np.ndarray):
+        assert x.dtype == np.float64 and x.strides[0] == 8, "column-major float64 array expected"
+        r, c = x.shape
+        return C.c_void_p(x.ctypes.data), r, c, max(x.strides[1] // 8 if c > 1 else r, r, 1)
+    assert x.dtype.itemsize == 8 and (x.stride(0) == 1 or x.numel() == 0), "column-major fp64 tensor expected"
+    r, c = x.shape
+    return C.c_void_p(x.data_ptr()), r, c, max(x.stride(1) if c > 1 else r, r, 1)
+
+
+def copy_matrix_async(dst, src, stream: int = 0) -> None:
+    """dst <- src between host and device memory (rutv_b200_copy_matrix_async), async on ``stream``."""
+    pd, r, c, ldd = _mat_ptr(dst)
+    ps, r2, c2, lds = _mat_ptr(src)
+    if (r, c) != (r2, c2):
+        raise ValueError("copy_matrix_async: shape mismatch")
+    st = Status()
+    lib().rutv_b200_copy_matrix_async(pd, ldd, ps, lds, r, c, stream, C.byref(st))
+    _raise(st)
 
 
 def launch_count() -> int:

@@ -288,6 +288,18 @@ int rutv_b200_host_alloc(size_t bytes, void** p, rutv_status* st) {
     });
 }
 
+int rutv_b200_copy_matrix_async(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                                int64_t cols, uint64_t stream, rutv_status* st) {
+    return guarded(st, [&] {
+        if (rows < 0 || cols < 0 || ldd < std::max<int64_t>(rows, 1) || lds < std::max<int64_t>(rows, 1))
+            throw Error(RUTV_ERR_SHAPE, "copy_matrix: bad shape or leading dimension");
+        if (rows * cols == 0) return;
+        RUTV_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(ldd) * 8, src, static_cast<size_t>(lds) * 8,
+                                    static_cast<size_t>(rows) * 8, static_cast<size_t>(cols), cudaMemcpyDefault,
+                                    reinterpret_cast<cudaStream_t>(stream)));
+    });
+}
+
 int rutv_b200_host_free(void* p, rutv_status* st) {
     return guarded(st, [&] {
         if (p) RUTV_CUDA(cudaFreeHost(p));

@@ -105,3 +105,28 @@ def test_cpp_dropin_header_compiles_and_links(tmp_path):
     and links librutv_b200.so (the drop-in of randutv_blocked.hpp:39)."""
     rutv.lib()
     assert os.path.exists(_build_shim(str(tmp_path / "shim")))
+
+
+def test_grid_local_shape_matches_python_grid():
+    """The C++ sharded driver's block-cyclic layout (dist.cu Axis) == dist.Grid
+    (block_cyclic.cpp:26-38), including ragged last blocks and ranks that own nothing."""
+    from paper_2104_05782_b200.dist import Grid
+    for n, b in [(1000, 128), (1024, 128), (50000, 512), (30000, 256), (300, 64), (5, 8), (0, 4)]:
+        for P, Q in [(1, 1), (1, 2), (2, 1), (2, 2), (2, 3), (2, 4), (3, 3), (1, 8)]:
+            tot_r = tot_c = 0
+            for rk in range(P * Q):
+                got = rutv.grid_local_shape(n, b, P, Q, rk)
+                assert got == Grid(n, b, P, Q, rk).local_shape(), (n, b, P, Q, rk)
+                if rk % Q == 0:
+                    tot_r += got[0]
+                if rk < Q:
+                    tot_c += got[1]
+            assert tot_r == n and tot_c == n
+    with pytest.raises(ValueError):
+        rutv.grid_local_shape(100, 8, 2, 2, 4)
+
+
+def test_opts_grid_fields_default_to_one_gpu():
+    o = rutv.make_opts()
+    assert (o.grid_p, o.grid_q, o.grid_sim) == (1, 1, 0)
+    assert C.sizeof(rutv.Opts) == 72  # the C struct rutv_opts
