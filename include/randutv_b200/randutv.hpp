@@ -111,6 +111,8 @@ struct UTVConfig {
     std::uint64_t seed = 0;
     bool qr_prepass = false;
     int device = 0;  // B200 addition: CUDA device ordinal
+    int grid_p = 1;  // B200 addition: shard over a grid_p x grid_q block-cyclic grid of GPUs
+    int grid_q = 1;  //   (devices 0 .. grid_p*grid_q - 1, NCCL; square inputs)
 };
 
 struct UTVResult {
@@ -146,6 +148,8 @@ inline UTVResult randutv(ConstMatrixView a, const UTVConfig& cfg) {
     o.seed = cfg.seed;
     o.qr_prepass = cfg.qr_prepass ? 1 : 0;
     o.device = cfg.device;
+    o.grid_p = cfg.grid_p;
+    o.grid_q = cfg.grid_q;
     UTVResult r;
     r.config = cfg;
     r.t = Matrix(a.rows, a.cols);
