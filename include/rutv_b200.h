@@ -66,8 +66,14 @@ typedef struct {
     int32_t grid_q;     /* GPUs; 1 x 1 = one GPU.  Host-pointer rutv_b200_factorize only (square). */
     int32_t grid_sim;   /* 1: run the grid's ranks as threads on o->device with an in-process      */
                         /*    exchange instead of NCCL (validation of the sharded path on 1 GPU)   */
-    int32_t reserved1;
+    int32_t keep_workspace; /* 1: leave this call's device workspace cached in the library's     */
+                            /*    pool (repeated calls of one size skip re-mapping it, e.g. 60 GB */
+                            /*    at n = 50000); rutv_b200_release_workspace() returns it.  0:   */
+                            /*    trimmed to RUTV_POOL_KEEP_MB (4 GB) when the call returns.      */
 } rutv_opts;
+
+/* Return every cached byte of the library's device pool on `device` to the driver. */
+int rutv_b200_release_workspace(int device);
 
 #define RUTV_NCCL_ID_BYTES 128
 

@@ -54,7 +54,7 @@ class Opts(C.Structure):
                 ("qr_prepass", C.c_int32), ("seed", C.c_uint64), ("device", C.c_int32),
                 ("max_steps", C.c_int32), ("overlap", C.c_int32), ("reserved0", C.c_int32),
                 ("stream", C.c_uint64), ("grid_p", C.c_int32), ("grid_q", C.c_int32),
-                ("grid_sim", C.c_int32), ("reserved1", C.c_int32)]
+                ("grid_sim", C.c_int32), ("keep_workspace", C.c_int32)]
 
 
 _D = C.POINTER(C.c_double)
@@ -84,6 +84,7 @@ def lib() -> C.CDLL:
     L.rutv_b200_factorize_device.argtypes = fac
     L.rutv_b200_last_profile.argtypes = [C.POINTER(C.c_char_p), _D, C.c_int]
     L.rutv_b200_launch_count.restype = C.c_uint64
+    L.rutv_b200_release_workspace.argtypes = [C.c_int]
     L.rutv_b200_normal_at.argtypes = [C.c_uint64, C.c_uint64]
     L.rutv_b200_normal_at.restype = C.c_double
     L.rutv_b200_build_v_alpha.argtypes = [C.c_int, C.c_void_p, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64,
@@ -167,11 +168,13 @@ def _raise(st: Status) -> None:
 
 def make_opts(b: int = 128, q: int = 1, seed: int = 0, build_u: bool = True, build_v: bool = True,
               qr_prepass: bool = False, device: int = 0, max_steps: int = -1,
-              overlap: bool = True, stream: int = 0, grid=(1, 1), grid_sim: bool = False) -> Opts:
+              overlap: bool = True, stream: int = 0, grid=(1, 1), grid_sim: bool = False,
+              keep_workspace: bool = False) -> Opts:
     o = Opts()
     lib().rutv_b200_default_opts(C.byref(o))
     o.grid_p, o.grid_q = int(grid[0]), int(grid[1])
     o.grid_sim = int(grid_sim)
+    o.keep_workspace = int(keep_workspace)
     o.b, o.q, o.seed = int(b), int(q), int(seed)
     o.build_u, o.build_v, o.qr_prepass = int(build_u), int(build_v), int(qr_prepass)
     o.device, o.max_steps, o.overlap = int(device), int(max_steps), int(overlap)
@@ -433,6 +436,11 @@ def copy_matrix_async(dst, src, stream: int = 0) -> None:
     st = Status()
     lib().rutv_b200_copy_matrix_async(pd, ldd, ps, lds, r, c, stream, C.byref(st))
     _raise(st)
+
+
+def release_workspace(device: int = 0) -> None:
+    """Return the library pool's cached device memory (kept by keep_workspace calls)."""
+    lib().rutv_b200_release_workspace(device)
 
 
 def launch_count() -> int:

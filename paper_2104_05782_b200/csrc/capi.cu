@@ -191,6 +191,7 @@ int rutv_b200_factorize(const rutv_opts* o, const double* A, int64_t m, int64_t 
     return guarded(st, [&] {
         check_opts(o);
         set_device(o->device);
+        rutv::pool_keep_this_call(o->keep_workspace != 0);
         Stream s(o->stream);
         const int64_t mm = std::max<int64_t>(m, 0), nn = std::max<int64_t>(n, 0);
         const bool prepass = o->qr_prepass && m > n;  // the inner n x n run draws the stream
@@ -263,10 +264,20 @@ int rutv_b200_factorize_device(const rutv_opts* o, const double* dA, int64_t m, 
     return guarded(st, [&] {
         check_opts(o);
         set_device(o->device);
+        rutv::pool_keep_this_call(o->keep_workspace != 0);
         Stream s(o->stream);
         run_factorize(o, dA, m, n, lda, dG, g_len, dT, ldt, dU, ldu, dV, ldv, s.s);
         RUTV_CUDA(cudaStreamSynchronize(s.s));
     });
+}
+
+int rutv_b200_release_workspace(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        return RUTV_ERR_CUDA;
+    }
+    rutv::pool_release(device);
+    return RUTV_OK;
 }
 
 int rutv_b200_last_profile(const char** names, double* ms, int cap) {

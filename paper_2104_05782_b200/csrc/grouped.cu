@@ -125,10 +125,14 @@ __global__ void __launch_bounds__(kGT, 1) small_mul_kernel(const SmallMulDesc* _
     }
 }
 
-// block_i := rect-diag(sigma_i) (randutv_blocked.cpp:32-37), one CTA per block
+// block_i := rect-diag(sigma_i) (randutv_blocked.cpp:32-37); blockIdx.y selects the
+// block, the x CTAs of a row stride over it (config 5's first block is 50000 x 512:
+// one CTA per block made the whole launch wait ~6 ms on it).
 __global__ void rect_diag_grouped_kernel(const RectDiagDesc* __restrict__ descs) {
-    const RectDiagDesc d = descs[blockIdx.x];
-    for (int64_t e = threadIdx.x; e < d.rows * d.cols; e += blockDim.x) {
+    const RectDiagDesc d = descs[blockIdx.y];
+    const int64_t total = d.rows * d.cols;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t r = e % d.rows, c = e / d.rows;
         d.A[r + c * d.ld] = (r == c && r < d.p) ? d.sigma[r] : 0.0;
     }
@@ -142,7 +146,12 @@ void rect_diag_grouped(cudaStream_t st, const std::vector<RectDiagDesc>& descs, 
     const size_t db = descs.size() * sizeof(RectDiagDesc);
     if (db > scratch_bytes) throw Error(RUTV_ERR_INTERNAL, "rect_diag_grouped: scratch too small");
     RUTV_CUDA(cudaMemcpyAsync(dev_scratch, descs.data(), db, cudaMemcpyHostToDevice, st));
-    rect_diag_grouped_kernel<<<static_cast<unsigned>(descs.size()), 1024, 0, st>>>(
+    int64_t most = 1;
+    for (const auto& d : descs) most = std::max(most, d.rows * d.cols);
+    // enough CTAs per block for the largest; a grid of about 8 waves overall
+    const int64_t per = std::min<int64_t>((most + 1023) / 1024,
+                                          std::max<int64_t>(1, 8 * kNumSMs / static_cast<int64_t>(descs.size())));
+    rect_diag_grouped_kernel<<<dim3(static_cast<unsigned>(per), static_cast<unsigned>(descs.size())), 1024, 0, st>>>(
         static_cast<const RectDiagDesc*>(dev_scratch));
     note_launch();
     RUTV_CHECK_LAUNCH();

@@ -79,7 +79,28 @@ void* dev_alloc(size_t bytes, cudaStream_t st) {
     return p;
 }
 
+namespace {
+thread_local bool t_keep = false;
+}
+
+void pool_keep_this_call(bool keep) { t_keep = keep; }
+
+void pool_release(int dev) {
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_pool_mu);
+        auto it = g_pools.find(dev);
+        if (it == g_pools.end()) return;
+        pool = it->second;
+    }
+    cudaMemPoolTrimTo(pool, 0);
+}
+
 void pool_trim() {
+    if (t_keep) {  // the caller asked to keep this call's workspace (rutv_opts.keep_workspace)
+        t_keep = false;
+        return;
+    }
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return;
     cudaMemPool_t pool = nullptr;

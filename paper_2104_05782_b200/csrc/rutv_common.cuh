@@ -65,6 +65,8 @@ enum class Op { N = 0, T = 1 };
 // public call returns all but RUTV_POOL_KEEP_MB (default 4096) to the driver.
 void* dev_alloc(size_t bytes, cudaStream_t st);
 void pool_trim();
+void pool_keep_this_call(bool keep);  // skip the trim that ends the current call (keep_workspace)
+void pool_release(int device);
 
 struct DevBuf {
     double* p = nullptr;

@@ -55,3 +55,25 @@ def test_missing_device_is_a_status_not_a_crash():
     assert ei.value.code == 5  # RUTV_ERR_CUDA
     t, u, v = rutv.factorize(a, b=8, q=1, seed=1)  # the library is still usable
     assert np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a) < 1e-13
+
+
+def test_keep_workspace_then_release():
+    """rutv_opts.keep_workspace leaves the call's workspace in the library pool (the next
+    call of the same size reuses it); rutv_b200_release_workspace returns it.  Results are
+    identical either way."""
+    import ctypes as C
+    import torch
+    n, b, q = 1200, 128, 1
+    a = oracle.gaussian_matrix(n, n, 21)
+    ref = rutv.factorize(a, b=b, q=q, seed=5)
+    o = rutv.make_opts(b=b, q=q, seed=5, keep_workspace=True)
+    outs = [np.zeros((n, n), order="F") for _ in range(3)]
+    st = rutv.Status()
+    free0 = torch.cuda.mem_get_info()[0]
+    rutv.lib().rutv_b200_factorize(C.byref(o), a.ctypes.data_as(C.c_void_p), n, n, n, None, 0,
+                                   *[x for h in outs for x in (h.ctypes.data_as(C.c_void_p), n)], C.byref(st))
+    rutv._raise(st)
+    for x, y in zip(outs, ref):
+        assert np.array_equal(x, y)
+    rutv.release_workspace(0)
+    assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)  # nothing left cached beyond slack
