@@ -349,6 +349,7 @@ struct Args {
 inline int64_t rup4(int64_t x) { return std::max<int64_t>((x + 3) / 4 * 4, 1); }
 
 void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
+    NvtxRange range("rutv/factorize_dist");
     const int64_t n = fa.n, b = fa.b;
     const int P = cx.P, Q = cx.Q, pr = cx.pr(), pc = cx.pc(), me = cx.rank;
     const Axis RA{n, b, P}, CA{n, b, Q};
@@ -363,12 +364,15 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
 
     // streams: critical chain on a high-priority stream A, V/U accumulation on B
     const bool overlap = fa.overlap;
-    cudaStream_t sA = st_in, sB = st_in;
+    // C: the panel-first look-ahead's remaining columns (one priority level below A)
+    cudaStream_t sA = st_in, sB = st_in, sC = st_in, sD = st_in;
     int lo = 0, hi = 0;
     RUTV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     if (overlap) {
         RUTV_CUDA(cudaStreamCreateWithPriority(&sA, cudaStreamNonBlocking, hi));
         RUTV_CUDA(cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, lo));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sC, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sD, cudaStreamNonBlocking, hi));
         cudaEvent_t e;
         RUTV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         RUTV_CUDA(cudaEventRecord(e, st_in));
@@ -384,7 +388,7 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
                 cudaStreamDestroy(s);
             }
         }
-    } gA{sA, overlap}, gB{sB, overlap};
+    } gA{sA, overlap}, gB{sB, overlap}, gC{sC, overlap}, gD{sD, overlap};
     std::vector<cudaEvent_t> events;
     struct EventGuard {
         std::vector<cudaEvent_t>& ev;
@@ -445,7 +449,7 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
     const int64_t gwe = std::max<int64_t>({gemm_work_elems(std::max(vr + mr, n), b, std::max(mr, mc)),
                                            gemm_work_elems(b, std::max<int64_t>(mc, 1), std::max<int64_t>(mr, 1)),
                                            gemm_work_elems(n, b, b), gemm_work_elems(b, b, n), int64_t(1)});
-    DevBuf GWA(gwe, sA), GWB(gwe, sA);
+    DevBuf GWA(gwe, sA), GWB(gwe, sA), GWC(gwe, sA), GWD(gwe, sA);
     const int64_t hqw = hqr_work_elems(n, b);
     DevBuf HQ(hqw, sA);
     // deferred beta: my diagonal steps' R, and the factor slots
@@ -470,17 +474,21 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
     {
         const cudaEvent_t ev = record(sA);
         wait(sB, ev);
+        wait(sC, ev);
+        wait(sD, ev);
     }
     struct Join {
-        cudaStream_t a, b;
+        cudaStream_t a, b, c, d;
         bool own;
         ~Join() {
             if (own) {
                 cudaStreamSynchronize(a);
                 cudaStreamSynchronize(b);
+                cudaStreamSynchronize(c);
+                cudaStreamSynchronize(d);
             }
         }
-    } join{sA, sB, overlap};
+    } join{sA, sB, sC, sD, overlap};
 
     auto gemmA = [&](double al, Op ta, const DView& x, Op tb, const DView& y, double be, const DView& c) {
         gemm(sA, al, ta, x, tb, y, be, c, GWA.p, gwe);
@@ -511,12 +519,17 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
         }
     };
     // W (unit lower), Twy, M = W Twy' of a packed s x b panel
+    // W (unit lower) on A; Twy (Gram + form_wy_t) and M = W Twy' on stream D, while A
+    // already runs the W-only half of the apply (X W, resp. W' B) -- as randutv.cu.
+    // Returns D's event (M ready).
     auto form_wy = [&](const double* qr, int64_t s, const double* tau, double* W, double* M) {
         DView Wv_(s, b, s, W), Mv_(s, b, s, M);
         make_w(sA, DView(s, b, s, const_cast<double*>(qr)), b, Wv_);
-        gemmA(1.0, Op::T, Wv_, Op::N, Wv_, 0.0, DView(b, b, b, Gram.p));
-        form_t(sA, Gram.p, b, tau, b, Twy.p, b);
-        gemmA(1.0, Op::N, Wv_, Op::T, DView(b, b, b, Twy.p), 0.0, Mv_);
+        wait(sD, record(sA));
+        gemm(sD, 1.0, Op::T, Wv_, Op::N, Wv_, 0.0, DView(b, b, b, Gram.p), GWD.p, gwe);
+        form_t(sD, Gram.p, b, tau, b, Twy.p, b);
+        gemm(sD, 1.0, Op::N, Wv_, Op::T, DView(b, b, b, Twy.p), 0.0, Mv_, GWD.p, gwe);
+        return record(sD);
     };
 
     uint64_t pos = 0;
@@ -568,10 +581,17 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
         // ---- QR(Y), redundantly on every rank (:52-53)
         gather(*cx.row, CA, i, s, Yl.p, std::max<int64_t>(m_c, 1), m_c, slabC, SlabY.p, SlabsY.p, Yf.p);
         hqr_panel(sA, DView(s, b, s, Yf.p), TauV.p, nullptr, 0, HQ.p, hqw);
-        form_wy(Yf.p, s, TauV.p, Wv.p, Mv.p);
+        const cudaEvent_t evMv = form_wy(Yf.p, s, TauV.p, Wv.p, Mv.p);
         // ---- V-apply (:140-143): T22 rows on A; V and finished T rows on B
+        if (m_c > 0) pick(sA, CA, pc, i, s, Wv.p, b, WlA.p, std::max<int64_t>(m_c, 1));
+        if (m_r > 0) {  // Zx = X W_v[my cols]: needs only W (D forms Twy_v, M_v meanwhile)
+            DView X = vt.block(vr + ri, ci, m_r, m_c), Zx(m_r, b, std::max<int64_t>(m_r, 1), ZxA.p);
+            if (m_c > 0) gemmA(1.0, Op::N, X, Op::N, DView(m_c, b, std::max<int64_t>(m_c, 1), WlA.p), 0.0, Zx);
+            else RUTV_CUDA(cudaMemsetAsync(ZxA.p, 0, static_cast<size_t>(m_r * b) * 8, sA));
+            cx.row->allreduce_sum(ZxA.p, static_cast<size_t>(m_r * b), sA);
+        }
+        wait(sA, evMv);
         if (m_c > 0) {
-            pick(sA, CA, pc, i, s, Wv.p, b, WlA.p, std::max<int64_t>(m_c, 1));
             pick(sA, CA, pc, i, s, Mv.p, b, MlA.p, std::max<int64_t>(m_c, 1));
             copy_view(sA, DView(m_c, b, std::max<int64_t>(mc, 1), WvB[par]), DView(m_c, b, std::max<int64_t>(m_c, 1), WlA.p));
             copy_view(sA, DView(m_c, b, std::max<int64_t>(mc, 1), MvB[par]), DView(m_c, b, std::max<int64_t>(m_c, 1), MlA.p));
@@ -579,12 +599,19 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
         const cudaEvent_t evV = record(sA);
         if (m_r > 0) {
             DView X = vt.block(vr + ri, ci, m_r, m_c), Zx(m_r, b, std::max<int64_t>(m_r, 1), ZxA.p);
-            DView Wl(m_c, b, std::max<int64_t>(m_c, 1), WlA.p), Ml(m_c, b, std::max<int64_t>(m_c, 1), MlA.p);
-            if (m_c > 0) gemmA(1.0, Op::N, X, Op::N, Wl, 0.0, Zx);
-            else RUTV_CUDA(cudaMemsetAsync(ZxA.p, 0, static_cast<size_t>(m_r * b) * 8, sA));
-            cx.row->allreduce_sum(ZxA.p, static_cast<size_t>(m_r * b), sA);
-            if (m_c > 0) gemmA(-1.0, Op::N, Zx, Op::T, Ml, 1.0, X);
+            DView Ml(m_c, b, std::max<int64_t>(m_c, 1), MlA.p);
+            // Panel-first look-ahead (as randutv.cu): the process column that holds block
+            // column i updates those b columns first on A -- all the panel QR needs --
+            // and every other column on C, beside the panel gather / QR / broadcast.
+            const int64_t c_first = (static_cast<int>(i % Q) == pc) ? std::min<int64_t>(b, m_c) : 0;
+            if (c_first > 0) gemmA(-1.0, Op::N, Zx, Op::T, Ml.block(0, 0, c_first, b), 1.0, X.block(0, 0, m_r, c_first));
+            if (m_c > c_first) {
+                wait(sC, record(sA));
+                gemm(sC, -1.0, Op::N, Zx, Op::T, Ml.block(c_first, 0, m_c - c_first, b), 1.0,
+                     X.block(0, c_first, m_r, m_c - c_first), GWC.p, gwe);
+            }
         }
+        const cudaEvent_t evRest = record(sC);  // the columns Q_u' needs besides the panel
         // ---- U-side panel QR (build_u_alpha, :58-64)
         const int pan_pc = static_cast<int>(i % Q);
         if (pc == pan_pc) gather(*cx.col, RA, i, s, T22.data, tl.ld, m_r, slabR, SlabP.p, SlabsP.p, Pan.p);
@@ -595,8 +622,9 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
         }
         cx.world->broadcast(Pan.p, static_cast<size_t>(s * b), downer, sA);
         cx.world->broadcast(TauU.p, static_cast<size_t>(b), downer, sA);
-        form_wy(Pan.p, s, TauU.p, Wu.p, Mu.p);
-        // ---- Q_u' on T22(:, b:) (:147)
+        const cudaEvent_t evMu = form_wy(Pan.p, s, TauU.p, Wu.p, Mu.p);
+        // ---- Q_u' on T22(:, b:) (:147): Zl = W_u' B needs only W (D forms M_u meanwhile)
+        wait(sA, evRest);
         {
             const int64_t c0 = pc == pan_pc ? b : 0;
             const int64_t nc = m_c - c0;
@@ -604,18 +632,21 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
                 DView Zl(b, nc, b, ZlA.p);
                 if (m_r > 0) {
                     pick(sA, RA, pr, i, s, Wu.p, b, WrA.p, std::max<int64_t>(m_r, 1));
-                    pick(sA, RA, pr, i, s, Mu.p, b, MrA.p, std::max<int64_t>(m_r, 1));
                     gemmA(1.0, Op::T, DView(m_r, b, std::max<int64_t>(m_r, 1), WrA.p), Op::N, T22.block(0, c0, m_r, nc),
                           0.0, Zl);
                 } else {
                     RUTV_CUDA(cudaMemsetAsync(ZlA.p, 0, static_cast<size_t>(b * nc) * 8, sA));
                 }
                 cx.col->allreduce_sum(ZlA.p, static_cast<size_t>(b * nc), sA);
-                if (m_r > 0)
+                wait(sA, evMu);
+                if (m_r > 0) {
+                    pick(sA, RA, pr, i, s, Mu.p, b, MrA.p, std::max<int64_t>(m_r, 1));
                     gemmA(-1.0, Op::N, DView(m_r, b, std::max<int64_t>(m_r, 1), MrA.p), Op::N, Zl, 1.0,
                           T22.block(0, c0, m_r, nc));
+                }
             }
         }
+        wait(sA, evMu);
         if (m_c > 0 && bu) {
             pick(sA, CA, pc, i, s, Wu.p, b, WuB[par], std::max<int64_t>(mc, 1));
             pick(sA, CA, pc, i, s, Mu.p, b, MuB[par], std::max<int64_t>(mc, 1));

@@ -288,7 +288,22 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
     uint64_t pos = 0;  // stream position P_i
     bool have_y = false;  // Y of this step formed by the previous one
     std::vector<cudaEvent_t> evB;
+    NvtxRange loop_range("rutv/steps");
+    // NVTX phase ranges of the step (host enqueue order; Nsight projects them onto the
+    // kernels launched inside): sketch / qr_v / apply_v / qr_u / apply_u / accumulate
+    struct Phase {
+        bool open = false;
+        void operator()(const char* name) {
+            if (open) nvtxRangePop();
+            nvtxRangePushA(name);
+            open = true;
+        }
+        ~Phase() {
+            if (open) nvtxRangePop();
+        }
+    };
     for (int i = 0; i < nsteps; ++i) {
+        Phase phase;
         const int64_t r0 = plan[static_cast<size_t>(i)].r0, s = plan[static_cast<size_t>(i)].s;
         DView t22 = tmat.block(r0, r0, s, s);
         double* Ri = Rall.p + static_cast<int64_t>(i) * bb * bb;
@@ -300,6 +315,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
         if (i >= 2) wait(st, evB[static_cast<size_t>(i - 2)]);  // slot `par` free again
         const bool hoist_next = hoist && i + 1 < nsteps && !plan[static_cast<size_t>(i + 1)].tail;
 
+        phase("rutv/sketch");
         // ---- sketch (build_v_alpha, randutv_blocked.cpp:41-50).  Y = T22' G was
         // already formed during the previous step when it was hoisted (below).
         DView Yv(s, b, s, Yb[par]), Zv(s, b, s, Z.p);
@@ -315,6 +331,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
             gemmA(1.0, Op::T, t22, Op::N, Zv, 0.0, Yv);
         }
         prof.mark(P_SKETCH);
+        phase("rutv/qr_v");
         // ---- V-side QR (:52-53)
         hqr_panel(st, Yv, tau.p, nullptr, 0, HQ.p, hqw);
         prof.mark(P_QRV);
@@ -336,6 +353,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
             evPan = record(st);  // panel columns updated: C may start (enqueued after QR_u)
         }
         prof.mark(P_APPLYV);
+        phase("rutv/qr_u");
         // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
         DView panel = t22.block(0, 0, s, b);
         hqr_panel(st, panel, tauU.p, nullptr, 0, HQ.p, hqw);
@@ -385,6 +403,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
         const cudaEvent_t evU = record(st);
         prof.mark(P_APPLYU);
 
+        phase("rutv/accumulate");
         // ======== stream B: V / U accumulation of step i ========
         wait(sB, evV);
         if (vr + r0 > 0) {  // V-apply on V and T(0:r0, r0:) (:141-143)
@@ -406,6 +425,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
     if (overlap) wait(st, record(sB));  // join
 
     // ======== deferred beta stage (:66-82, :129-137, :150-154) ========
+    NvtxRange beta_range("rutv/deferred_beta");
     if (nsteps > 0) {
         std::vector<SvdDesc> descs(static_cast<size_t>(nsteps));
         int64_t nmax = 0;
@@ -549,6 +569,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
 }
 
 void factorize_device(cudaStream_t st_in, int device, int64_t n, const FactorArgs& fa) {
+    NvtxRange range("rutv/factorize");
     if (cholqr_deferred_enabled() && factorize_impl(st_in, device, n, fa, true)) return;
     factorize_impl(st_in, device, n, fa, false);
 }

@@ -15,9 +15,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rutv_b200.h"
 
 namespace rutv {
+
+// NVTX range for profilers (Nsight Systems / ncu --nvtx): free when no tool is attached.
+// The factorization marks each step and phase (tracing).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kNumSMs = 148;  // B200; queried at runtime for sizing decisions
 

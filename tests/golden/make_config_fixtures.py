@@ -15,6 +15,8 @@ config2  n=4000, A = geometric_matrix(n, n, 10^(-12/3999), seedA=1) (metrics.cpp
          the reference's own invariants (residual, orthogonality in three norms) and a
          SHA-256 of A's bytes (the test regenerates A with the C port and checks the hash,
          so both sides factor bit-identical input).
+config4shape  the same first-step fixture at config 4's n = 30000, b = 256, q = 2 (Gaussian A:
+         config 4's cliff matrix comes from the GPU Haar generator); ~40 min on one core.
 config3  n=10000 Gaussian A (metrics.cpp:90-93, seedA=1), b=256, q=1, seedG=2: the reference's
          state after its FIRST step through the public step API (ref_randutv_steps, the
          randutv() loop replayed on build_v_alpha / apply_q_right / build_u_alpha /
@@ -97,8 +99,8 @@ def config2(verify_a: bool) -> None:
         **{f"ref_{k}": val for k, val in inv.items()})
 
 
-def config3() -> None:
-    n, b, q, seed_a, seed_g = 10000, 256, 1, 1, 2
+def config3(n=10000, b=256, q=1, name="config3_step1_ref.npz") -> None:
+    seed_a, seed_g = 1, 2
     t0 = time.time()
     a = oracle.gaussian_matrix(n, n, seed_a)
     print(f"A {time.time() - t0:.1f} s", flush=True)
@@ -113,7 +115,7 @@ def config3() -> None:
     ti = rng.integers(b, n, 30000)
     tj = rng.integers(b, n, 30000)
     np.savez_compressed(
-        os.path.join(OUT, "config3_step1_ref.npz"),
+        os.path.join(OUT, name),
         n=n, b=b, q=q, seed_a=seed_a, seed_g=seed_g, a_sha256=sha(a),
         diag=np.diag(t)[:b].copy(), strip_cols=cols, strip=t[:b, cols],
         rows=rows, u_rows=u[rows, :b], v_rows=v[rows, :b],
@@ -126,5 +128,7 @@ if __name__ == "__main__":
     what = sys.argv[1:] or ["config2", "config3"]
     if "config3" in what:
         config3()
+    if "config4shape" in what:  # config 4's n, b, q on a Gaussian A (its cliff A needs the GPU generator)
+        config3(30000, 256, 2, "config4shape_step1_ref.npz")
     if "config2" in what:
         config2("--verify-a" in what)
