@@ -20,9 +20,12 @@
 //     deterministic split-K for the skinny K = s products (one side = b);
 //   * split-K partials are summed in a fixed order by a separate kernel, so
 //     results are bit-reproducible run to run.
-// Measured (tools/gemm_bench.py, profiles/r01_gemm_sweep.jsonl): 32.5 TF/s at
-// 8192^3 (88% of the DMMA peak; cuBLAS's sm_80 d884 kernel 35.5), 21.7 at the
-// rank-128 update 4000^2 x 128, 30.5 at 20000^2 x 512.
+// Measured (tools/gemm_bench.py, tools/gemm_c5.py; DESIGN.md GEMM table): 34.5 TF/s
+// at 8192^3 (93 % of the DMMA peak; cuBLAS's sm_80 d884 kernel 35.5), 33.3 at the
+// config-5 rank-512 update 50000^2 x 512 (cuBLAS 27.8), 35.1 at the config-5 sketch
+// 50000 x 512 x 50000 (cuBLAS 36.2), 25.0 at the rank-128 update 4000^2 x 128.
+// Tried and measured slower: 128 x 128 tiles on one CTA per SM (29.4 at the config-5
+// update), 4 pipeline stages, red.global.add epilogues for beta = 1.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
