@@ -535,6 +535,15 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
     uint64_t pos = 0;
     int64_t steps = 0, tail_w = 0;
     std::vector<cudaEvent_t> evB;
+    // Sketch hoisting (as randutv.cu): the next step's first sketch product is formed
+    // from B = (T22 Q_v)(my rows >= i+1, my cols >= i+1) -- final once the V-apply is
+    // done -- on stream C beside the panel QR: P = B' G'_loc, corrected after Q_u' by
+    // - Zl' (M_u(my rows >= i+1)' G'_loc), since T22' = B - M_u Zl on those rows.  The
+    // corrected partial is what the next step all-reduces (mathematically T22'^T G').
+    const char* hoist_env = std::getenv("RUTV_HOIST");
+    const bool hoist = overlap && !(hoist_env && std::strcmp(hoist_env, "0") == 0);
+    bool have_y = false;
+    DevBuf G2(std::max<int64_t>(mr, 1) * b, sA), Mh(std::max<int64_t>(mr, 1) * b, sA), Hh(b * b, sA);
     for (int64_t i = 0; i < nblk; ++i) {
         if (fa.max_steps >= 0 && steps >= fa.max_steps) break;
         const int64_t s = n - i * b;
@@ -555,7 +564,7 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
         if (i >= 2) wait(sA, evB[static_cast<size_t>(i - 2)]);  // B done with slot `par`
         // ---- sketch (build_v_alpha, :41-50)
         DView G(m_r, b, std::max<int64_t>(m_r, 1), Gl.p), Y(m_c, b, std::max<int64_t>(m_c, 1), Yl.p), Z(m_r, b, std::max<int64_t>(m_r, 1), Zr.p);
-        if (m_r > 0) {
+        if (m_r > 0 && !have_y) {
             const int64_t k0 = RA.first_from(i, pr);
             if (fa.dG)
                 block_rows(sA, G.data, G.ld, const_cast<double*>(fa.dG) + pos, s, s, b, b, k0 - i, P,
@@ -565,9 +574,12 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
         }
         pos += static_cast<uint64_t>(s * b);
         if (m_c > 0) {
-            gemmA(1.0, Op::T, T22, Op::N, G, 0.0, Y);
+            // hoisted: Yl already holds this rank's partial of T22' G (formed during the
+            // previous step beside its panel QR); otherwise the plain product
+            if (!have_y) gemmA(1.0, Op::T, T22, Op::N, G, 0.0, Y);
             cx.col->allreduce_sum(Yl.p, static_cast<size_t>(m_c * b), sA);
         }
+        have_y = false;
         for (int it = 0; it < fa.q; ++it) {
             if (m_r > 0) {
                 gemmA(1.0, Op::N, T22, Op::N, Y, 0.0, Z);
@@ -612,6 +624,30 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
             }
         }
         const cudaEvent_t evRest = record(sC);  // the columns Q_u' needs besides the panel
+        // ---- sketch hoisting: P = B' G'_loc on stream C, beside the panel QR
+        const bool hoist_next =
+            hoist && i + 1 < nblk && n - (i + 1) * b > b && (fa.max_steps < 0 || steps < fa.max_steps);
+        cudaEvent_t evP = nullptr;
+        const int64_t ri1 = RA.suffix(i + 1, pr).first, ci1 = CA.suffix(i + 1, pc).first;
+        const int64_t mr1 = mr - ri1, nc1 = mc - ci1;
+        if (hoist_next) {
+            const int64_t s1 = s - b;
+            wait(sC, record(sA));
+            if (mr1 > 0) {
+                const int64_t k1 = RA.first_from(i + 1, pr);
+                if (fa.dG)
+                    block_rows(sC, G2.p, mr1, const_cast<double*>(fa.dG) + pos, s1, s1, b, b, k1 - (i + 1), P,
+                               RA.suffix(i + 1, pr).second, false);
+                else
+                    normal_fill_cyclic(sC, fa.seed, pos, s1, b, k1 - (i + 1), P, DView(mr1, b, mr1, G2.p));
+            }
+            if (nc1 > 0) {
+                const DView Bl = mr1 > 0 ? tl.block(ri1, ci1, mr1, nc1) : DView(0, nc1, tl.ld, tl.data);
+                gemm(sC, 1.0, Op::T, Bl, Op::N, DView(mr1, b, std::max<int64_t>(mr1, 1), G2.p), 0.0,
+                     DView(nc1, b, nc1, Yl.p), GWC.p, gwe);
+            }
+            evP = record(sC);
+        }
         // ---- U-side panel QR (build_u_alpha, :58-64)
         const int pan_pc = static_cast<int>(i % Q);
         if (pc == pan_pc) gather(*cx.col, RA, i, s, T22.data, tl.ld, m_r, slabR, SlabP.p, SlabsP.p, Pan.p);
@@ -639,6 +675,7 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
                 }
                 cx.col->allreduce_sum(ZlA.p, static_cast<size_t>(b * nc), sA);
                 wait(sA, evMu);
+                wait(sA, evP);  // the hoisted P read B before this update
                 if (m_r > 0) {
                     pick(sA, RA, pr, i, s, Mu.p, b, MrA.p, std::max<int64_t>(m_r, 1));
                     gemmA(-1.0, Op::N, DView(m_r, b, std::max<int64_t>(m_r, 1), MrA.p), Op::N, Zl, 1.0,
@@ -647,6 +684,21 @@ void factorize_rank(Ctx& cx, const Args& fa, cudaStream_t st_in) {
             }
         }
         wait(sA, evMu);
+        if (hoist_next) {  // Y'_partial = P - Zl' (M_u(my rows >= i+1)' G'_loc)
+            wait(sA, evP);
+            if (nc1 > 0) {
+                if (mr1 > 0) {
+                    const int64_t k1 = RA.first_from(i + 1, pr);
+                    block_rows(sA, Mh.p, mr1, Mu.p + b, s, s - b, b, b, k1 - (i + 1), P, RA.suffix(i + 1, pr).second,
+                               false);
+                }
+                gemmA(1.0, Op::T, DView(mr1, b, std::max<int64_t>(mr1, 1), Mh.p), Op::N,
+                      DView(mr1, b, std::max<int64_t>(mr1, 1), G2.p), 0.0, DView(b, b, b, Hh.p));
+                gemmA(-1.0, Op::T, DView(b, nc1, b, ZlA.p), Op::N, DView(b, b, b, Hh.p), 1.0,
+                      DView(nc1, b, nc1, Yl.p));
+            }
+            have_y = true;
+        }
         if (m_c > 0 && bu) {
             pick(sA, CA, pc, i, s, Wu.p, b, WuB[par], std::max<int64_t>(mc, 1));
             pick(sA, CA, pc, i, s, Mu.p, b, MuB[par], std::max<int64_t>(mc, 1));
