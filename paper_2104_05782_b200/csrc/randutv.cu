@@ -144,10 +144,19 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
     // host synchronisation on A, so the results are complete on return.
     // Stream D (high priority) forms Twy and M = W Twy' of each panel while A
     // already runs the big W-only product of the apply (X W, resp. W' B).
-    cudaStream_t st = st_in, sB = st_in, sC = st_in, sD = st_in;
+    // Stream E (low priority), RUTV_SVD_STREAM=1 only: each step's b x b Jacobi SVD is
+    // launched as soon as its R is saved, beside the following steps, instead of the one
+    // batched launch after the loop.  Measured 3x SLOWER (config 1 15.9 -> 52.3 ms,
+    // config 2 49.1 -> 97.0 ms): a resident Jacobi cluster holds its SMs for ~3 ms, and
+    // the 16-CTA panel-QR clusters on the critical chain cannot be placed in a GPC until
+    // it leaves.  Kept as an experiment switch; the batched launch is the product.
+    const char* sv_env = std::getenv("RUTV_SVD_STREAM");
+    const bool svd_per_step = sv_env && std::strcmp(sv_env, "0") != 0;
+    cudaStream_t st = st_in, sB = st_in, sC = st_in, sD = st_in, sE = st_in;
     if (overlap) {
         int prio_lo = 0, prio_hi = 0;
         RUTV_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        RUTV_CUDA(cudaStreamCreateWithPriority(&sE, cudaStreamNonBlocking, prio_lo));
         RUTV_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio_hi));
         // C (look-ahead GEMMs that run beside the panel QR) one level below A:
         // a pending QR cluster must not wait behind C's CTAs for its 16 SMs.
@@ -170,7 +179,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
                 cudaStreamDestroy(s);
             }
         }
-    } sguardA{st, overlap}, sguard{sB, overlap}, sguardC{sC, overlap}, sguardD{sD, overlap};
+    } sguardA{st, overlap}, sguard{sB, overlap}, sguardC{sC, overlap}, sguardD{sD, overlap}, sguardE{sE, overlap};
     if (prof_overlap) {  // re-anchor the timeline on the critical stream
         prof.st = st;
         prof.mark(P_START);
@@ -231,6 +240,30 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
     const int64_t desc_words = (static_cast<int64_t>(sizeof(SvdDesc)) * ns + 7) / 8;
     DevBuf Ddesc(desc_words, st);
     RUTV_CUDA(cudaMemsetAsync(Jst.p, 0, static_cast<size_t>(ns) * 32, st));
+    // every step's SVD problem descriptor (known from the plan), uploaded once
+    int64_t svd_nmax = 0;
+    if (nsteps > 0) {
+        std::vector<SvdDesc> descs(static_cast<size_t>(nsteps));
+        for (int i = 0; i < nsteps; ++i) {
+            const StepInfo& si = plan[static_cast<size_t>(i)];
+            const int64_t w = si.tail ? si.s : b;
+            svd_nmax = std::max(svd_nmax, w);
+            const int64_t off = static_cast<int64_t>(i) * bb * bb;
+            descs[static_cast<size_t>(i)] =
+                SvdDesc{Rall.p + off, w, static_cast<int>(w), 0, Usall.p + off,
+                        Sall.p + static_cast<int64_t>(i) * (bb + 1), Vsall.p + off,
+                        SvdW.p + static_cast<int64_t>(i) * svdw, Jst.p + 4 * i};
+        }
+        RUTV_CUDA(cudaMemcpyAsync(Ddesc.p, descs.data(), sizeof(SvdDesc) * descs.size(), cudaMemcpyHostToDevice,
+                                  st));
+        RUTV_CUDA(cudaStreamSynchronize(st));  // the host vector dies at this scope's end
+    }
+    const SvdDesc* ddesc = reinterpret_cast<const SvdDesc*>(Ddesc.p);
+    auto launch_svd = [&](int i, int64_t w) {  // step i's Jacobi on stream E, after R_i is saved
+        if (!svd_per_step) return;
+        wait(sE, record(st));
+        svd_batch(sE, ddesc + i, 1, static_cast<int>(w), 1e-15, 30);
+    };
     const int64_t gw_elems =
         std::max<int64_t>({gemm_work_elems(n, bb, n), gemm_work_elems(bb, n, n), gemm_work_elems(vr + n, bb, n),
                            gemm_work_elems(bb, bb, n), gemm_work_elems(bb, n, bb), gemm_work_elems(vr + n, bb, bb),
@@ -251,11 +284,12 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
         wait(sB, ev);
         wait(sC, ev);
         wait(sD, ev);
+        wait(sE, ev);
     }
     // declared after every buffer -> destroyed first: stream B drains before any
     // buffer is released (also on the exception path)
     struct JoinGuard {
-        cudaStream_t a, s, c, d;
+        cudaStream_t a, s, c, d, e;
         bool own;
         ~JoinGuard() {
             if (own) {
@@ -263,9 +297,10 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
                 cudaStreamSynchronize(s);
                 cudaStreamSynchronize(c);
                 cudaStreamSynchronize(d);
+                cudaStreamSynchronize(e);
             }
         }
-    } jguard{st, sB, sC, sD, overlap};
+    } jguard{st, sB, sC, sD, sE, overlap};
 
     auto gemmA = [&](double alpha, Op ta, const DView& a, Op tb, const DView& bm, double beta,
                      const DView& c) { gemm(st, alpha, ta, a, tb, bm, beta, c, GWA.p, gw_elems); };
@@ -309,6 +344,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
         double* Ri = Rall.p + static_cast<int64_t>(i) * bb * bb;
         if (plan[static_cast<size_t>(i)].tail) {  // ragged tail: dense s x s block (:129-137)
             copy_view(st, DView(s, s, s, Ri), t22);
+            launch_svd(i, s);
             break;
         }
         const int par = i & 1;
@@ -382,6 +418,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
         }
         const cudaEvent_t evTu = form_wy(panel, b, tauU.p, Wu[par], Mu[par]);
         copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
+        launch_svd(i, b);
         prof.mark(P_WYU);
         DView WuV(s, b, s, Wu[par]), MuV(s, b, s, Mu[par]);
         wait(st, evR);
@@ -427,21 +464,10 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
     // ======== deferred beta stage (:66-82, :129-137, :150-154) ========
     NvtxRange beta_range("rutv/deferred_beta");
     if (nsteps > 0) {
-        std::vector<SvdDesc> descs(static_cast<size_t>(nsteps));
-        int64_t nmax = 0;
-        for (int i = 0; i < nsteps; ++i) {
-            const StepInfo& si = plan[static_cast<size_t>(i)];
-            const int64_t w = si.tail ? si.s : b;
-            nmax = std::max(nmax, w);
-            const int64_t off = static_cast<int64_t>(i) * bb * bb;
-            descs[static_cast<size_t>(i)] =
-                SvdDesc{Rall.p + off, w, static_cast<int>(w), 0, Usall.p + off,
-                        Sall.p + static_cast<int64_t>(i) * (bb + 1), Vsall.p + off,
-                        SvdW.p + static_cast<int64_t>(i) * svdw, Jst.p + 4 * i};
-        }
-        RUTV_CUDA(cudaMemcpyAsync(Ddesc.p, descs.data(), sizeof(SvdDesc) * descs.size(),
-                                  cudaMemcpyHostToDevice, st));
-        svd_batch(st, reinterpret_cast<const SvdDesc*>(Ddesc.p), nsteps, static_cast<int>(nmax), 1e-15, 30);
+        if (svd_per_step)
+            wait(st, record(sE));  // the per-step Jacobis (launched during the loop) are done
+        else
+            svd_batch(st, ddesc, nsteps, static_cast<int>(svd_nmax), 1e-15, 30);
         prof.mark(P_SVD);
         const cudaEvent_t evS = record(st);
         // Products with the SVD factors: one grouped in-place launch per kind
