@@ -317,6 +317,21 @@ void split_groups(Ctx& cx, ncclComm_t world) {
     cx.row = wrap(row);
     cx.col = wrap(col);
     cx.row_side = wrap(side);
+    // One tiny collective per communicator, in a fixed order, synchronously: NCCL sets up
+    // its buffers and connections lazily at a communicator's first collective, and that
+    // must not happen later while the other communicator has a kernel in flight on
+    // another stream of this rank.
+    double* one = nullptr;
+    cudaStream_t s = nullptr;
+    RUTV_CUDA(cudaMalloc(reinterpret_cast<void**>(&one), 8));
+    RUTV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    RUTV_CUDA(cudaMemsetAsync(one, 0, 8, s));
+    for (Group* g : {cx.world.get(), cx.row.get(), cx.col.get(), cx.row_side.get()}) {
+        g->allreduce_sum(one, 1, s);
+        RUTV_CUDA(cudaStreamSynchronize(s));
+    }
+    cudaStreamDestroy(s);
+    cudaFree(one);
 }
 
 void sim_groups(Ctx& cx, SimHub* hub) {
