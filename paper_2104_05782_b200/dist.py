@@ -1,4 +1,14 @@
-"""Multi-GPU blocked randUTV over a 2D block-cyclic P x Q grid.
+"""Multi-GPU blocked randUTV over a 2D block-cyclic P x Q grid --
+the Python model of the schedule.
+
+The PRODUCT multi-GPU path is the C++ driver ``csrc/dist.cu`` behind the C ABI
+(``rutv_b200_factorize_dist``, ``rutv_opts.grid_p/q``; ``bench.py --gpus N``), which
+restates this algorithm with the single-GPU driver's overlap (panel-first look-ahead,
+sketch hoisting, Twy/M on a side stream).  This module keeps the same algorithm over
+torch.distributed with a pluggable ``ops`` object, so the distributed schedule itself
+is testable on the CPU with gloo (tests/test_dist_cpu.py) and, through ``CudaOps``,
+with NCCL (tests/test_gpu_dist.py); ``Grid`` is also the reference the C++ layout is
+checked against (tests/test_capi.py).
 
 One process per GPU (torch.distributed, NCCL on the GPU path).  The layout is
 the paper's ScaLAPACK scheme with the distribution block
