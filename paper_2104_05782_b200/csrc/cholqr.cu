@@ -616,6 +616,17 @@ bool immediate_enabled() {
 
 thread_local int* t_deferred_flag = nullptr;
 
+// Tall sub-panels take the fast path by default (immediate mode): rows per
+// panel from which Cholesky-QR2 beats the cluster Householder kernel
+// (RUTV_CHOLQR_MIN_ROWS, 0 = never).
+int64_t tall_min_rows() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("RUTV_CHOLQR_MIN_ROWS");
+        return e ? std::atoll(e) : static_cast<int64_t>(6144);
+    }();
+    return v;
+}
+
 void gemm_w(cudaStream_t st, double alpha, Op ta, const DView& a, Op tb, const DView& b, double beta,
             const DView& c) {
     const int64_t k = ta == Op::N ? a.cols : a.rows;
@@ -641,10 +652,12 @@ bool cholqr_deferred_enabled() {
 
 void cholqr_set_deferred(int* dflag) { t_deferred_flag = dflag; }
 
+bool cholqr_tall(int64_t s) { return tall_min_rows() > 0 && s >= tall_min_rows(); }
+
 bool qr_panel_fast(cudaStream_t st, const DView& y, double* tau) {
     const int64_t s = y.rows, p = y.cols;
     int* dflag = t_deferred_flag;
-    if (!dflag && !immediate_enabled()) return false;
+    if (!dflag && !immediate_enabled() && !cholqr_tall(s)) return false;
     if (p < 16 || p > 128 || s < 2 * p) return false;
     small_attr();
     const size_t smb = small_smem_bytes(static_cast<int>(p));

@@ -381,11 +381,21 @@ void launch_cluster(cudaStream_t stream, const DView& a, double* tau, int cs) {
 
 }  // namespace
 
-int64_t hqr_work_elems(int64_t s, int64_t w) {
+namespace {
+// one blocked right-looking pass with sub-panels of at most nb columns
+int64_t blocked_work_elems(int64_t s, int64_t w, int64_t nbmax) {
     // W (s x nb) + Gram (nb x nb) + Tsub (nb x nb) + Z, Z2 (nb x w) + gemm split-K scratch
-    const int64_t nb = std::min<int64_t>(w, 512);
+    const int64_t nb = std::min<int64_t>(w, nbmax);
     return s * nb + 2 * nb * nb + 2 * nb * w + gemm_work_elems(nb, w, s) +
            gemm_work_elems(nb, nb, s) + 1024;
+}
+constexpr int64_t kFastCols = 128;  // sub-panel width of the Cholesky-QR2 path (cholqr.cu)
+}  // namespace
+
+int64_t hqr_work_elems(int64_t s, int64_t w) {
+    // the Householder kernels' own blocking, plus (tall panels, cholqr_tall) the outer
+    // loop over 128-column fast sub-panels whose fallback runs the former inside
+    return blocked_work_elems(s, w, 512) + blocked_work_elems(s, std::min(w, kFastCols), 512);
 }
 
 // qr_reg.cu: micro-panel register kernel (preferred where its chunk fits)
@@ -403,11 +413,57 @@ bool reg_kernel_enabled() {
 }
 }  // namespace
 
+namespace {
+// Blocked right-looking panel QR: sub-panels of nb columns factored by `factor`,
+// trailing update A_trail <- (I - W T W')' A_trail = A_trail - W T' (W' A_trail).
+template <class Factor>
+void blocked_panel(cudaStream_t stream, const DView& a, double* tau, int64_t nb, double* scratch,
+                   int64_t scratch_elems, Factor factor) {
+    const int64_t s = a.rows, w = a.cols, p = std::min(s, w);
+    double* W = scratch;
+    double* Gm = W + s * nb;
+    double* Ts = Gm + nb * nb;
+    double* Z = Ts + nb * nb;
+    double* Z2 = Z + nb * w;
+    double* gw = Z2 + nb * w;
+    const int64_t gw_elems = scratch_elems - (gw - scratch);
+    if (gw_elems < 0) throw Error(RUTV_ERR_INTERNAL, "hqr: scratch too small");
+    for (int64_t j0 = 0; j0 < p; j0 += nb) {
+        const int64_t jb = std::min(nb, p - j0);
+        DView sub = a.block(j0, j0, s - j0, jb);
+        factor(sub, tau + j0);
+        const int64_t rest = w - j0 - jb;
+        if (rest <= 0) continue;
+        DView trail = a.block(j0, j0 + jb, s - j0, rest);
+        DView Wv(s - j0, jb, s - j0, W);
+        make_w(stream, sub, jb, Wv);
+        DView Gv(jb, jb, jb, Gm), Tv(jb, jb, jb, Ts);
+        gemm(stream, 1.0, Op::T, Wv, Op::N, Wv, 0.0, Gv, gw, gw_elems);
+        form_t(stream, Gm, jb, tau + j0, jb, Ts, jb);
+        DView Zv(jb, rest, jb, Z), Z2v(jb, rest, jb, Z2);
+        gemm(stream, 1.0, Op::T, Wv, Op::N, trail, 0.0, Zv, gw, gw_elems);
+        gemm(stream, 1.0, Op::T, Tv, Op::N, Zv, 0.0, Z2v, gw, gw_elems);
+        gemm(stream, -1.0, Op::N, Wv, Op::N, Z2v, 1.0, trail, gw, gw_elems);
+    }
+}
+}  // namespace
+
 void hqr_panel(cudaStream_t stream, const DView& a, double* tau, double* twy, int64_t ldt,
                double* scratch, int64_t scratch_elems) {
     const int64_t s = a.rows, w = a.cols, p = std::min(s, w);
     if (p == 0) return;
-    if (!qr_panel_fast(stream, a, tau)) hqr_panel_householder(stream, a, tau, scratch, scratch_elems);
+    if (w > kFastCols && cholqr_tall(s) && scratch_elems >= hqr_work_elems(s, w)) {
+        // Tall panel: 128-column sub-panels by Cholesky-QR2 + Householder reconstruction
+        // (level-3 work on every SM instead of one 16-CTA cluster streaming the panel
+        // column by column), each falling back to the Householder kernels when unsafe.
+        const int64_t outer = blocked_work_elems(s, w, 512);
+        blocked_panel(stream, a, tau, kFastCols, scratch, outer, [&](const DView& sub, double* t) {
+            if (!qr_panel_fast(stream, sub, t))
+                hqr_panel_householder(stream, sub, t, scratch + outer, scratch_elems - outer);
+        });
+    } else if (!qr_panel_fast(stream, a, tau)) {
+        hqr_panel_householder(stream, a, tau, scratch, scratch_elems);
+    }
     if (twy) {
         // Twy of the whole panel: Gram of W then the forward recurrence.
         if (scratch_elems < s * p + p * p) throw Error(RUTV_ERR_INTERNAL, "hqr: scratch too small");
@@ -445,33 +501,8 @@ void hqr_panel_householder(cudaStream_t stream, const DView& a, double* tau, dou
     if (cap >= w && w <= 512) {
         launch(a, tau);
     } else {
-        // Blocked right-looking: sub-panels of nb columns, trailing update
-        // A_trail <- (I - W T W')' A_trail = A_trail - W T' (W' A_trail).
         const int64_t nb = std::min<int64_t>(512, use_reg ? cap : std::max<int64_t>(1, (cap / 8) * 8 > 0 ? (cap / 8) * 8 : cap));
-        double* W = scratch;
-        double* Gm = W + s * nb;
-        double* Ts = Gm + nb * nb;
-        double* Z = Ts + nb * nb;
-        double* Z2 = Z + nb * w;
-        double* gw = Z2 + nb * w;
-        const int64_t gw_elems = scratch_elems - (gw - scratch);
-        for (int64_t j0 = 0; j0 < p; j0 += nb) {
-            const int64_t jb = std::min(nb, p - j0);
-            DView sub = a.block(j0, j0, s - j0, jb);
-            launch(sub, tau + j0);
-            const int64_t rest = w - j0 - jb;
-            if (rest <= 0) continue;
-            DView trail = a.block(j0, j0 + jb, s - j0, rest);
-            DView Wv(s - j0, jb, s - j0, W);
-            make_w(stream, sub, jb, Wv);
-            DView Gv(jb, jb, jb, Gm), Tv(jb, jb, jb, Ts);
-            gemm(stream, 1.0, Op::T, Wv, Op::N, Wv, 0.0, Gv, gw, gw_elems);
-            form_t(stream, Gm, jb, tau + j0, jb, Ts, jb);
-            DView Zv(jb, rest, jb, Z), Z2v(jb, rest, jb, Z2);
-            gemm(stream, 1.0, Op::T, Wv, Op::N, trail, 0.0, Zv, gw, gw_elems);
-            gemm(stream, 1.0, Op::T, Tv, Op::N, Zv, 0.0, Z2v, gw, gw_elems);
-            gemm(stream, -1.0, Op::N, Wv, Op::N, Z2v, 1.0, trail, gw, gw_elems);
-        }
+        blocked_panel(stream, a, tau, nb, scratch, scratch_elems, launch);
     }
 }
 

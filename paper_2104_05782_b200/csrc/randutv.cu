@@ -392,10 +392,7 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
         phase("rutv/qr_u");
         // ---- U-side QR of the panel, in place (build_u_alpha, :58-64)
         DView panel = t22.block(0, 0, s, b);
-        hqr_panel(st, panel, tauU.p, nullptr, 0, HQ.p, hqw);
-        prof.mark(P_QRU);
-        {  // stream C, enqueued after the QR_u launch so the QR cluster gets its SMs
-           // before C's CTAs fill the GPU: the other s-b columns of the V-apply
+        auto stream_c_work = [&] {  // the other s-b columns of the V-apply, then the hoisted sketch
             DView X = vt.block(vr + r0, r0, s, s);
             DView Zx(s, b, s, ZxA.p);
             wait(sC, evPan);
@@ -415,7 +412,15 @@ static bool factorize_impl(cudaStream_t st_in, int device, int64_t n, const Fact
                      gw_elems);
             }
             evR = record(sC);
-        }
+        };
+        // Stream C is enqueued after the QR_u launch so the QR cluster gets its SMs before
+        // C's CTAs fill the GPU -- except for tall panels, whose Cholesky-QR2 sub-panels
+        // synchronise the host with stream A (safety flag): there C must already be queued.
+        const bool c_first = overlap && cholqr_tall(s);
+        if (c_first) stream_c_work();
+        hqr_panel(st, panel, tauU.p, nullptr, 0, HQ.p, hqw);
+        prof.mark(P_QRU);
+        if (!c_first) stream_c_work();
         const cudaEvent_t evTu = form_wy(panel, b, tauU.p, Wu[par], Mu[par]);
         copy_upper(st, DView(b, b, b, Ri), t22.block(0, 0, b, b));  // beta_stage's R (:73-75)
         launch_svd(i, b);

@@ -173,6 +173,11 @@ bool qr_panel_fast(cudaStream_t stream, const DView& a, double* tau);
 // without a host check and OR their safety flags into *dflag (null: off).
 void cholqr_set_deferred(int* dflag);
 bool cholqr_deferred_enabled();
+// Panels of at least this many rows take the fast path by default, in
+// immediate mode: the safety flag is read back after each <= 128-column
+// sub-panel (one host synchronisation of the panel's stream) and an unsafe
+// sub-panel is redone by the Householder kernels.
+bool cholqr_tall(int64_t s);
 
 // One-sided Jacobi SVD of a square block (jacobi_svd.cpp:39-148).  Writes U, sigma, V
 // (n x n, ld n).  Status (code, residual, kept, sweeps) is written to
