@@ -32,6 +32,16 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
                  "r"(rbar)
                  : "memory");
 }
+// The same for two consecutive doubles (16-byte aligned remote address): half the remote
+// stores -- the CTA's remote-store rate (~1 per cycle) bounds the larger exchanges.
+__device__ __forceinline__ void st_async_v2f64(uint32_t raddr, double v0, double v1, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "d"(v0), "d"(v1), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void lds_v2f64(uint32_t a, double& v0, double& v1) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(a));
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

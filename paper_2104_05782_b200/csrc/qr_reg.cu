@@ -33,6 +33,26 @@
 //
 // Rows per thread MR = 1 or 2 (chunk rows R <= 1024); taller chunks use the
 // one-level kernel.
+//
+// Micro-panel fast path ("CQ", default on; RUTV_QR_CQ=0 disables).  The column
+// loop above costs one cluster-wide exchange per column (~2.5 K cycles each).
+// A full 16-column micro-panel X (rows >= j0) with a well-conditioned Gram
+// matrix is instead factored with TWO exchanges, by Cholesky-QR2 and
+// Householder reconstruction (cholqr.cu's scheme at micro-panel granularity,
+// entirely in shared memory / registers):
+//   G = X'X (DMMA partials, all-gathered)        -> R1 = chol(G) in one warp
+//   X1 = X R1^-1 (per-row forward substitution in registers)
+//   E = X1'X1 - I (second exchange, with the 16 x 16 head block of X1)
+//   R2 = I + U1, U1 = striu(E) + diag(E)/2 (|E| <= 1e-9: the series is exact
+//   to 1e-18), Q = X1 (I - U1), R = R2 R1
+//   I - Q(head) = L U (one warp)  ->  V = [L; -Q(below) U^-1], tau = diag(U)
+// which are the reference's reflectors (beta >= 0 makes the thin QR unique) up
+// to rounding.  Every CTA forms bit-identical G / E (fixed summation order), so
+// the safety decisions are uniform across the cluster: Cholesky breakdown or
+// min/max diag(R1) < 1e-3 -> the micro-panel takes the column loop with its
+// registers untouched; |E| > 1e-9 or an LU pivot |tau_j| < 0.25 (a reflector
+// near the identity, e.g. tau = 0) -> X is restored as X1 R1 and the column
+// loop runs.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -40,6 +60,7 @@
 #include <cstdlib>
 
 #include "cluster_msg.cuh"
+#include "small_chains.cuh"
 #include "rutv_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -52,34 +73,49 @@ constexpr int kT = 512;       // threads per CTA
 constexpr int kWarps = kT / 32;
 constexpr int KB = 16;        // micro-panel width
 constexpr int kMsg = 2 * KB;  // per-column message: 16 partial dots + 16 head-row entries
+constexpr int kNG = KB * (KB + 1) / 2;  // packed upper triangle of a 16 x 16 Gram matrix
+constexpr int kCqMat = KB * KB;         // one 16 x 16 matrix
+constexpr int kCqDoubles = 5 * kCqMat + 2 * kNG + 2 * KB + 2;  // rmat, rfin, lumat, q1in, q1 staging, 2 Gram staging, rdinv, udinv, flags
 constexpr unsigned kFull = 0xffffffffu;
 
 struct RegSmem {
     double* chunk;  // w x LD, column-major
     double* msg;    // [2][CS][kMsg]
-    double* rsb;    // [CS][KB][nsmax] reduce-scatter inbox
+    double* rsb;    // [CS][KB][nsmax] reduce-scatter inbox; also the CQ hop-1 inbox [CS][kNG]
+    double* gin2;   // [CS][kNG] CQ hop-2 inbox
+    double* cq;     // CQ small matrices (kCqDoubles)
     double* zg;     // [KB][ncol] all-gathered V'[V | A_t], then -T'Z in place
     double* part;   // per-warp partials: column dots [kWarps][KB]; block [ksplit][KB][ncol]
     double* tmat;   // [KB][KB] T, row-major
     double* taus;   // [KB]
     double* hsend;  // [KB] head row of the next column (row owner only)
-    uint64_t* bar;  // [4]: column parity 0/1, reduce-scatter, all-gather
+    uint64_t* bar;  // [6]: column parity 0/1, reduce-scatter, all-gather, CQ hop 1, CQ hop 2
 };
 
 __host__ __device__ inline int ns_max(int w, int cs) { return (KB + w + cs - 1) / cs; }
 __host__ __device__ inline int part_elems(int w) { return KB * std::max(kWarps * 8, KB + w); }
 
+// The hop-1 inbox of the CQ path shares the reduce-scatter inbox: a peer enters the block
+// phase of micro-panel m only after every CTA's hop-2 message of m (sent after that CTA read
+// its hop-1 inbox), and sends hop 1 of m + 1 only after the all-gather of block phase m, which
+// every CTA feeds after consuming its reduce-scatter inbox.
+__host__ __device__ inline int rs_elems(int w, int cs) { return std::max(cs * KB * ns_max(w, cs), cs * kNG); }
+// even, so the buffers behind the chunk stay 16-byte aligned (16-byte remote stores)
+__host__ __device__ inline size_t chunk_elems(int w, int LD) { return (static_cast<size_t>(w) * LD + 1) & ~static_cast<size_t>(1); }
+
 __host__ __device__ inline size_t reg_smem_doubles(int w, int LD, int cs) {
-    return static_cast<size_t>(w) * LD + 2 * cs * kMsg + static_cast<size_t>(cs) * KB * ns_max(w, cs) +
-           static_cast<size_t>(KB) * (KB + w) + part_elems(w) + KB * KB + 2 * KB + 4;
+    return static_cast<size_t>(chunk_elems(w, LD)) + 2 * cs * kMsg + static_cast<size_t>(rs_elems(w, cs)) + cs * kNG +
+           kCqDoubles + static_cast<size_t>(KB) * (KB + w) + part_elems(w) + KB * KB + 2 * KB + 6;
 }
 
 __device__ __forceinline__ RegSmem carve(double* sm, int w, int LD, int CS) {
     RegSmem S;
     S.chunk = sm;
-    S.msg = S.chunk + static_cast<size_t>(w) * LD;
+    S.msg = S.chunk + chunk_elems(w, LD);
     S.rsb = S.msg + 2 * CS * kMsg;
-    S.zg = S.rsb + static_cast<size_t>(CS) * KB * ns_max(w, CS);
+    S.gin2 = S.rsb + rs_elems(w, CS);
+    S.cq = S.gin2 + CS * kNG;
+    S.zg = S.cq + kCqDoubles;
     S.part = S.zg + static_cast<size_t>(KB) * (KB + w);
     S.tmat = S.part + part_elems(w);
     S.taus = S.tmat + KB * KB;
@@ -112,7 +148,8 @@ __device__ int g_qr_ablate = 0;
 
 template <int MR>
 __global__ void __launch_bounds__(kT, 1)
-    hqr_reg_kernel(double* A, int64_t lda, int s, int w, int p, int R, int LD, double* tau, long long* trace) {
+    hqr_reg_kernel(double* A, int64_t lda, int s, int w, int p, int R, int LD, double* tau, long long* trace,
+                   int cq_mode) {
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = static_cast<int>(cluster.num_blocks());
     const int rank = static_cast<int>(cluster.block_rank());
@@ -146,14 +183,23 @@ __global__ void __launch_bounds__(kT, 1)
             if (jj + min(KB, w - jj) < w) return jj;
         return -1;
     };
+    // CQ exchanges: hop 1 = CS packed Gram partials; hop 2 = the same plus the 16 x 16 head block
+    const uint32_t hop1_bytes = static_cast<uint32_t>(CS * kNG * 8);
+    const uint32_t hop2_bytes = static_cast<uint32_t>((CS * kNG + kCqMat) * 8);
     if (tid == 0) {
-        for (int b = 0; b < 4; ++b) mbar_init(&S.bar[b], 1);
+        for (int b = 0; b < 6; ++b) mbar_init(&S.bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0) {
-        if (p > 0) mbar_arm(&S.bar[0], col_bytes);
-        if (p > 1) mbar_arm(&S.bar[1], col_bytes);
+        // The column barriers 0/1 are armed per micro-panel (only the micro-panels that take
+        // the column loop use them); the CQ barriers once here and again after every
+        // completed wait.  A message may land before its barrier is armed: the phase only
+        // completes with the arming thread's own arrival.
+        if (cq_mode) {
+            mbar_arm(&S.bar[4], hop1_bytes);
+            mbar_arm(&S.bar[5], hop2_bytes);
+        }
         const int f = (0 + min(KB, w) < w && p > 0) ? 0 : next_phase_j0(0);
         if (nphase > 0 && f >= 0) {
             mbar_arm(&S.bar[2], rs_bytes(f));
@@ -207,6 +253,94 @@ __global__ void __launch_bounds__(kT, 1)
 
     double x[MR][KB];
     int phase = 0;
+    // parities of the completed phases: bit 0 / 1 column barriers 0 / 1, bit 2 / 3 CQ hops 1 / 2
+    unsigned phbits = 0;
+    // CQ small matrices (16 x 16, row-major) by 32-bit shared addresses off one base
+    constexpr uint32_t kRmat = 0;                     // R1(k, j) at [16 k + j]
+    constexpr uint32_t kRfin = 8u * kCqMat;           // final R = (I + U1) R1
+    constexpr uint32_t kLumat = 16u * kCqMat;         // I - Q(head), then its packed LU
+    constexpr uint32_t kQ1in = 24u * kCqMat;          // head block of X1 (hop 2)
+    constexpr uint32_t kQ1st = 32u * kCqMat;          // staging of my head rows of X1
+    constexpr uint32_t kStg = 40u * kCqMat;           // staging of my packed Gram partial, hop 1 / hop 2
+    constexpr uint32_t kRdinv = kStg + 16u * kNG;     // 1 / R1(k, k)
+    constexpr uint32_t kUdinv = kRdinv + 8u * KB;     // 1 / U(k, k)
+    constexpr uint32_t kFlag = kUdinv + 8u * KB;      // int [0] pass 1, [1] LU
+    auto lds_i32 = [](uint32_t a) {
+        int v;
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+        return v;
+    };
+    auto sts_i32 = [](uint32_t a, int v) { asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); };
+    // this thread's packed Gram entry (i <= k), tid < kNG: pe = 16 i + k
+    int pe = 0;
+    if (tid < kNG) {
+        int k = 0;
+        while ((k + 1) * (k + 2) / 2 <= tid) ++k;
+        pe = (tid - k * (k + 1) / 2) * KB + k;
+    }
+    auto packed_index = [&](int& pi, int& pk) {
+        pi = pe >> 4;
+        pk = pe & 15;
+    };
+    // Packed Gram partial of chunk columns [j0, j0 + 16) over the local rows [lo, rc), summed
+    // over the warps in a fixed order and sent to every CTA's inbox (slot = my rank).
+    auto gram_send = [&](int j0, int lo, double* inbox, int barid) {
+        const int nk4 = (rc - lo + 3) >> 2;
+        const int k0 = (warp * nk4) / kWarps, k1 = ((warp + 1) * nk4) / kWarps;
+        double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};  // G(:, 0:8), G(:, 8:16)
+        const uint32_t p0 = chunk_a + 8u * static_cast<uint32_t>((j0 + g) * LD + lo + t4);
+        const uint32_t p1 = p0 + 8u * static_cast<uint32_t>(8 * LD);
+        for (int k4 = k0; k4 < k1; ++k4) {
+            const bool ok = lo + 4 * k4 + t4 < rc;  // a row past rc reads valid shared memory, selected away
+            const uint32_t o = 32u * static_cast<uint32_t>(k4);
+            const double r0 = lds_f64(p0 + o), r1 = lds_f64(p1 + o);
+            const double v0 = ok ? r0 : 0.0, v1 = ok ? r1 : 0.0;  // X(row, g), X(row, g + 8)
+            dmma(c0, v0, v1, v0);
+            dmma(c1, v0, v1, v1);
+        }
+        const bool gt = trace && tid == 0 && rank == 0 && (j0 >> 4) < 8 && barid == 4;
+        if (gt) trace[72 * 8 + (j0 >> 4) * 16 + 12] = clock64();
+        // 16 warp partials in 8 slots: warps 0-7 store, warps 8-15 add
+        double* slot = S.part + (warp & 7) * kCqMat;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            if ((warp >> 3) == half) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int idx = (g + (r >= 2 ? 8 : 0)) * KB + 2 * t4 + (r & 1);
+                    if (half == 0) {
+                        slot[idx] = c0[r];
+                        slot[idx + 8] = c1[r];
+                    } else {
+                        slot[idx] += c0[r];
+                        slot[idx + 8] += c1[r];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        const uint32_t stg = smem_u32(S.cq) + kStg + (barid == 5 ? 8u * kNG : 0u);
+        if (gt) trace[72 * 8 + (j0 >> 4) * 16 + 13] = clock64();
+        if (tid < kNG) {
+            double v = 0.0;
+#pragma unroll
+            for (int ws = 0; ws < 8; ++ws) v += lds_f64(part_a + 8u * static_cast<uint32_t>(ws * kCqMat + pe));
+            sts_f64(stg + 8u * tid, v);
+        }
+        if (gt) trace[72 * 8 + (j0 >> 4) * 16 + 14] = clock64();
+        __syncthreads();
+        if (gt) trace[72 * 8 + (j0 >> 4) * 16 + 15] = clock64();
+        // 68 pairs x CS destinations spread over all threads (16-byte remote stores: the CTA's
+        // remote-store rate bounds this exchange; a bulk DSMEM copy per destination was
+        // measured slower -- ~1.2 K cycles to issue behind a proxy fence)
+        const uint32_t inbox_a = smem_u32(inbox) + 8u * static_cast<uint32_t>(rank * kNG);
+        for (int idx = tid; idx < (kNG / 2) * CS; idx += kT) {
+            const int dst = idx / (kNG / 2), pr = idx - dst * (kNG / 2);
+            double a, b;
+            lds_v2f64(stg + 16u * pr, a, b);
+            st_async_v2f64(mapa_u32(inbox_a + 16u * pr, dst), a, b, mapa_u32(bar0 + 8 * barid, dst));
+        }
+    };
     for (int j0 = 0; j0 < p; j0 += KB) {
         const int kb = min(KB, p - j0), kt = min(KB, w - j0);
         // ---- load the micro-panel tile into registers.  The tile is a window
@@ -221,11 +355,198 @@ __global__ void __launch_bounds__(kT, 1)
             for (int k = 0; k < KB; ++k)
                 x[m][k] = (li < rc && k < kt) ? S.chunk[static_cast<size_t>(j0 + k) * LD + li] : 0.0;
         }
+        // ---- CQ fast path for a full micro-panel (see the header); hh = the column loop runs
+        bool hh = true;
+        if (cq_mode && kb == KB && kt == KB && s - j0 >= 2 * KB) {
+            const int lo = min(rc, max(0, j0 - r_beg));  // local rows with gi >= j0
+            const uint32_t cq_a = smem_u32(S.cq), tmat_a = smem_u32(S.tmat);
+            int pe_i = 0, pe_k = 0;
+            if (tid < kNG) packed_index(pe_i, pe_k);
+            const bool force1 = cq_mode == 3 && ((j0 >> 4) & 1), force2 = cq_mode == 2 && ((j0 >> 4) & 1);
+            const bool cqt = trace && tid == 0 && rank == 0 && (j0 >> 4) < 8;
+#define CQT(k) \
+    if (cqt) trace[72 * 8 + (j0 >> 4) * 16 + (k)] = clock64()
+            CQT(0);
+            // -- pass 1: G = X'X, R1 = chol(G)
+            gram_send(j0, lo, S.rsb, 4);
+            CQT(1);
+            mbar_wait(&S.bar[4], (phbits >> 2) & 1u);
+            phbits ^= 4u;
+            CQT(2);
+            if (tid == 0) mbar_arm(&S.bar[4], hop1_bytes);
+            if (tid < kNG) {
+                double v = 0.0;
+                for (int src = 0; src < CS; ++src) v += S.rsb[src * kNG + tid];
+                S.tmat[pe_i * KB + pe_k] = v;
+                S.tmat[pe_k * KB + pe_i] = v;
+            }
+            __syncthreads();
+            CQT(3);
+            if (warp == 0) {
+                const int kk = lane & (KB - 1);
+                double v[KB];
+#pragma unroll
+                for (int i = 0; i < KB; ++i) v[i] = S.tmat[i * KB + kk];
+                double mn, mx;
+                const bool brk = warp_chol16(v, cq_a + kRmat, cq_a + kRdinv, part_a, mn, mx, lane);
+                if (lane == 0) sts_i32(cq_a + kFlag, (brk || !(mn > 1e-3 * mx) || force1) ? 1 : 0);
+            }
+            __syncthreads();
+            CQT(4);
+            if (lds_i32(cq_a + kFlag) == 0) {
+                // -- X1 = X R1^-1 by rows (registers), mirrored into the chunk for the second Gram
+#pragma unroll
+                for (int m = 0; m < MR; ++m) {
+                    const int li = tid + kT * m;
+                    if (li >= lo && li < rc) {
+#pragma unroll
+                        for (int k = 0; k < KB; ++k) {
+                            const double yk = x[m][k] * lds_f64(cq_a + kRdinv + 8u * k);
+                            x[m][k] = yk;
+#pragma unroll
+                            for (int j = k + 1; j < KB; ++j)
+                                x[m][j] = __fma_rn(-yk, lds_f64(cq_a + kRmat + 8u * (k * KB + j)), x[m][j]);
+                        }
+                        const int hr = r_beg + li - j0;  // head-block row, if < 16
+#pragma unroll
+                        for (int k = 0; k < KB; ++k) {
+                            sts_f64(chunk_a + 8u * static_cast<uint32_t>((j0 + k) * LD + li), x[m][k]);
+                            if (hr < KB) sts_f64(cq_a + kQ1st + 8u * (hr * KB + k), x[m][k]);
+                        }
+                    }
+                }
+                __syncthreads();
+                CQT(5);
+                // -- pass 2: E = X1'X1 - I, with the head block of X1 from its owner(s)
+                gram_send(j0, lo, S.gin2, 5);
+                {  // my head rows [h0, h1) of X1 to every CTA
+                    const int h0 = max(0, r_beg - j0), h1 = min(KB, r_beg + rc - j0);
+                    const int npr = max(0, h1 - h0) * (KB / 2);
+                    for (int idx = tid; idx < npr * CS; idx += kT) {
+                        const int dst = idx / npr, pr = h0 * (KB / 2) + idx - dst * npr;
+                        double a, b;
+                        lds_v2f64(cq_a + kQ1st + 16u * pr, a, b);
+                        st_async_v2f64(mapa_u32(cq_a + kQ1in + 16u * pr, dst), a, b, mapa_u32(bar0 + 8 * 5, dst));
+                    }
+                }
+                CQT(6);
+                mbar_wait(&S.bar[5], (phbits >> 3) & 1u);
+                CQT(7);
+                phbits ^= 8u;
+                if (tid == 0) mbar_arm(&S.bar[5], hop2_bytes);
+                bool bad = false;
+                if (tid < kNG) {
+                    double v = 0.0;
+                    for (int src = 0; src < CS; ++src) v += S.gin2[src * kNG + tid];
+                    const double e = v - (pe_i == pe_k ? 1.0 : 0.0);
+                    S.tmat[pe_i * KB + pe_k] = e;
+                    S.tmat[pe_k * KB + pe_i] = e;
+                    bad = !(fabs(e) <= 1e-9);
+                }
+                bool redo = __syncthreads_or(bad || force2) != 0;
+                CQT(8);
+                if (!redo) {
+                    // -- Q(head) = X1(head) (I - U1), B = I - Q(head); R = (I + U1) R1
+                    if (tid < kCqMat) {
+                        const int r = tid >> 4, k = tid & 15;
+                        double acc = lds_f64(cq_a + kQ1in + 8u * (r * KB + k)) * (1.0 - 0.5 * lds_f64(tmat_a + 8u * (k * KB + k)));
+                        for (int i = 0; i < k; ++i)
+                            acc = __fma_rn(-lds_f64(cq_a + kQ1in + 8u * (r * KB + i)), lds_f64(tmat_a + 8u * (i * KB + k)), acc);
+                        sts_f64(cq_a + kLumat + 8u * (r * KB + k), (r == k ? 1.0 : 0.0) - acc);
+                    } else {
+                        const int i = (tid - kCqMat) >> 4, k = tid & 15;
+                        double acc = 0.0;
+                        if (i <= k) {
+                            acc = lds_f64(cq_a + kRmat + 8u * (i * KB + k)) * (1.0 + 0.5 * lds_f64(tmat_a + 8u * (i * KB + i)));
+                            for (int m2 = i + 1; m2 <= k; ++m2)
+                                acc = __fma_rn(lds_f64(tmat_a + 8u * (i * KB + m2)), lds_f64(cq_a + kRmat + 8u * (m2 * KB + k)), acc);
+                        }
+                        sts_f64(cq_a + kRfin + 8u * (i * KB + k), acc);
+                    }
+                    __syncthreads();
+                    CQT(9);
+                    if (warp == 0) {
+                        const int kk = lane & (KB - 1);
+                        double v[KB];
+#pragma unroll
+                        for (int i = 0; i < KB; ++i) v[i] = lds_f64(cq_a + kLumat + 8u * (i * KB + kk));
+                        __syncwarp();
+                        // tau = diag(U) lands in S.taus (the block phase's T recurrence reads it)
+                        const bool brk = warp_lu16(v, cq_a + kLumat, cq_a + kUdinv, smem_u32(S.taus), part_a, lane);
+                        const bool any = __any_sync(kFull, brk);
+                        if (lane == 0) sts_i32(cq_a + kFlag + 4u, any ? 1 : 0);
+                    }
+                    __syncthreads();
+                    CQT(10);
+                    redo = lds_i32(cq_a + kFlag + 4u) != 0;
+                }
+                if (!redo) {
+                    if (rank == 0 && tid < KB) tau[j0 + tid] = S.taus[tid];
+                    // -- V = [L; -Q(below) U^-1], R into the head rows; retire the micro-panel
+#pragma unroll
+                    for (int m = 0; m < MR; ++m) {
+                        const int li = tid + kT * m;
+                        if (li >= lo && li < rc) {
+                            const int hr = r_beg + li - j0;
+                            if (hr >= KB) {
+                                // y = x (I - U1), descending so x(i < k) is still X1
+#pragma unroll
+                                for (int k = KB - 1; k >= 0; --k) {
+                                    double acc = x[m][k] * (1.0 - 0.5 * lds_f64(tmat_a + 8u * (k * KB + k)));
+#pragma unroll
+                                    for (int i = 0; i < k; ++i)
+                                        acc = __fma_rn(-x[m][i], lds_f64(tmat_a + 8u * (i * KB + k)), acc);
+                                    x[m][k] = acc;
+                                }
+                                // z U = -y
+#pragma unroll
+                                for (int k = 0; k < KB; ++k) {
+                                    const double zk = -x[m][k] * lds_f64(cq_a + kUdinv + 8u * k);
+                                    x[m][k] = zk;
+#pragma unroll
+                                    for (int j = k + 1; j < KB; ++j)
+                                        x[m][j] = __fma_rn(zk, lds_f64(cq_a + kLumat + 8u * (k * KB + j)), x[m][j]);
+                                }
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < KB; ++k)
+                                    x[m][k] = lds_f64(cq_a + (k >= hr ? kRfin : kLumat) + 8u * (hr * KB + k));
+                            }
+#pragma unroll
+                            for (int k = 0; k < KB; ++k)
+                                sts_f64(chunk_a + 8u * static_cast<uint32_t>((j0 + k) * LD + li), x[m][k]);
+                        }
+                    }
+                    hh = false;
+                    CQT(11);
+                } else {
+                    // -- unsafe after pass 1: X = X1 R1 (descending, in place), then the column loop
+#pragma unroll
+                    for (int m = 0; m < MR; ++m) {
+                        const int li = tid + kT * m;
+                        if (li >= lo && li < rc) {
+#pragma unroll
+                            for (int j = KB - 1; j >= 0; --j) {
+                                double acc = 0.0;
+#pragma unroll
+                                for (int k = 0; k <= j; ++k)
+                                    acc = __fma_rn(x[m][k], lds_f64(cq_a + kRmat + 8u * (k * KB + j)), acc);
+                                x[m][j] = acc;
+                            }
+                        }
+                    }
+                }
+            }
+        }
         // ---- column steps, row-owning warps only (no CTA-wide barrier).
         // Every such warp waits for the column's message itself, sums the CS
         // partials in rank order and evaluates house() redundantly (identical
         // in every warp of the cluster), lane k forming w_k.
-        if (warp < nwact) {
+        if (hh && warp < nwact) {
+            if (tid == 0) {
+                mbar_arm(&S.bar[0], col_bytes);
+                if (kb > 1) mbar_arm(&S.bar[1], col_bytes);
+            }
             {  // partials of column j0: x_j0' x_{j0+k} over rows > j0, head row j0
                 double vals[KB];
 #pragma unroll
@@ -248,7 +569,7 @@ __global__ void __launch_bounds__(kT, 1)
                 const int j = j0 + c, par = j & 1;
                 const bool tr = trace && tid == 0 && rank == 0 && j < 64;
                 if (tr) trace[j * 8 + 0] = clock64();
-                mbar_wait(&S.bar[par], static_cast<uint32_t>((j >> 1) & 1));
+                mbar_wait(&S.bar[par], ((phbits >> par) + static_cast<unsigned>(c >> 1)) & 1u);
                 if (tr) trace[j * 8 + 1] = clock64();
                 double tsum;
                 {
@@ -344,7 +665,7 @@ __global__ void __launch_bounds__(kT, 1)
                     x[m][KB - 1] = 0.0;
                 }
                 if (tid == 0) {  // off the critical chain: re-arm slot par, record tau
-                    if (j + 2 < p) mbar_arm(&S.bar[par], col_bytes);
+                    if (c + 2 < kb) mbar_arm(&S.bar[par], col_bytes);
                     if (rank == 0) tau[j] = tj;
                     S.taus[c] = tj;
                 }
@@ -362,11 +683,12 @@ __global__ void __launch_bounds__(kT, 1)
                 }
             }
         }
+        if (hh) phbits ^= static_cast<unsigned>(((kb + 1) >> 1) & 1) | (static_cast<unsigned>((kb >> 1) & 1) << 1);
         // ---- tile columns beyond the factorised ones (wide panels, p < w)
 #pragma unroll
         for (int m = 0; m < MR; ++m) {
             const int li = tid + kT * m;
-            if (li < rc) {
+            if (hh && li < rc) {
 #pragma unroll
                 for (int k = 0; k < KB; ++k)
                     if (k < kt - kb) S.chunk[static_cast<size_t>(j0 + kb + k) * LD + li] = x[m][k];
@@ -630,18 +952,25 @@ void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
         return v;
     }();
     (void)ablate;
+    // RUTV_QR_CQ: 0 = column loop only, 1 (default) = CQ micro-panels; debug: 2 / 3 force the
+    // pass-2 / pass-1 fallback on every odd micro-panel
+    static const int cq_mode = [] {
+        const char* e = std::getenv("RUTV_QR_CQ");
+        return e ? std::atoi(e) : 1;
+    }();
     long long* trace = nullptr;
     if (tracing) {
-        RUTV_CUDA(cudaMalloc(&trace, 72 * 8 * sizeof(long long)));
-        RUTV_CUDA(cudaMemset(trace, 0, 72 * 8 * sizeof(long long)));
+        RUTV_CUDA(cudaMalloc(&trace, 88 * 8 * sizeof(long long)));
+        RUTV_CUDA(cudaMemset(trace, 0, 88 * 8 * sizeof(long long)));
     }
     if (R <= kT)
-        RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<1>, a.data, a.ld, s, w, p, R, LD, tau, trace));
+        RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<1>, a.data, a.ld, s, w, p, R, LD, tau, trace, cq_mode));
     else
-        RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<2>, a.data, a.ld, s, w, p, R, LD, tau, trace));
+        RUTV_CUDA(cudaLaunchKernelEx(&cfg, hqr_reg_kernel<2>, a.data, a.ld, s, w, p, R, LD, tau, trace, cq_mode));
     note_launch();
     if (tracing) {
-        long long h[72 * 8];
+        long long h[88 * 8];
+        RUTV_CUDA(cudaStreamSynchronize(stream));
         RUTV_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
         cudaFree(trace);
         std::fprintf(stderr, "qr_reg trace s=%d w=%d cs=%d (cycles: wait, house, update, reduce, send, next)\n", s, w, cs);
@@ -650,6 +979,16 @@ void qr_reg_launch(cudaStream_t stream, const DView& a, double* tau, int cs) {
             std::fprintf(stderr, "  col %2d: %6lld %6lld %6lld %6lld %6lld %6lld\n", j, r[1] - r[0], r[2] - r[1],
                          r[3] - r[2], h[(j + 1) * 8 + 4] - r[3], h[(j + 1) * 8 + 5] - h[(j + 1) * 8 + 4],
                          h[(j + 1) * 8 + 0] - h[(j + 1) * 8 + 5]);
+        }
+        std::fprintf(stderr,
+                     "  CQ micro-panels (cycles: gram1, hop1, sum, chol, solve, gram2, hop2, E, products, LU, rows)\n");
+        for (int mp = 0; mp < 8; ++mp) {
+            const long long* r = h + 72 * 8 + mp * 16;
+            if (!r[0]) continue;
+            std::fprintf(stderr, "  mp %d:", mp);
+            for (int k = 1; k < 12; ++k) std::fprintf(stderr, " %6lld", r[k] ? r[k] - r[k - 1] : -1LL);
+            std::fprintf(stderr, " | gram1: dmma %lld slots %lld reduce+fence %lld sync %lld issue %lld\n", r[12] - r[0],
+                         r[13] - r[12], r[14] - r[13], r[15] - r[14], r[1] - r[15]);
         }
         std::fprintf(stderr, "  block phases (cycles: partials, reduce-scatter, all-gather, T, Y, update)\n");
         for (int ph = 0; ph < 8; ++ph) {

@@ -16,6 +16,7 @@ __global__ void k(double* out, long long* cyc, double a, double b, int n) {
     if (MODE == 4) x = __drcp_rn(x + a);
     if (MODE == 5) x = __shfl_xor_sync(0xffffffffu, x, 1) + 0.0;
     if (MODE == 6) x = __shfl_xor_sync(0xffffffffu, x, 1);
+    if (MODE == 9) x = rsqrt(x + a);
     if (MODE == 7) {  // dependent mma.sync m16n8k4 f64 chain (accumulator dependency)
       double c0 = x, c1 = x, c2 = x, c3 = x;
       asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
@@ -34,9 +35,9 @@ __global__ void k(double* out, long long* cyc, double a, double b, int n) {
 
 int main() {
   double* o; long long* c; cudaMalloc(&o, 1024 * 8); cudaMalloc(&c, 8);
-  const char* names[] = {"dfma", "dadd", "ddiv", "dsqrt", "drcp_rn", "shfl+dadd", "shfl", "mma16x8x4+dadd", "mma8x8x4"};
+  const char* names[] = {"dfma", "dadd", "ddiv", "dsqrt", "drcp_rn", "shfl+dadd", "shfl", "mma16x8x4+dadd", "mma8x8x4", "drsqrt"};
   const int n = 4096;
-  for (int m = 0; m < 9; ++m) {
+  for (int m = 0; m < 10; ++m) {
     long long h = 0;
     for (int rep = 0; rep < 2; ++rep) {
       switch (m) {
@@ -49,6 +50,7 @@ int main() {
         case 6: k<6><<<1, 32>>>(o, c, 1.5, 1.0, n); break;
         case 7: k<7><<<1, 32>>>(o, c, 1e-3, 1e-3, n); break;
         case 8: k<8><<<1, 32>>>(o, c, 1e-3, 1e-3, n); break;
+        case 9: k<9><<<1, 32>>>(o, c, 1.5, 1.0, n); break;
       }
       cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
     }
