@@ -49,6 +49,25 @@ def test_grid_matches_single_gpu_device_rng():
     assert np.max(np.abs(u2 - u1 * d)) < 1e-9 and np.max(np.abs(v2 - v1 * d)) < 1e-9
 
 
+def test_grid_tall_panels_match_single_gpu():
+    """n above RUTV_CHOLQR_MIN_ROWS (6144): every rank factors the gathered sketch and the
+    diagonal owner the panel through the Cholesky-QR2 sub-panels, each reading its safety flag
+    back with a host synchronisation of its own critical stream -- inside the rank threads of
+    the in-process grid.  Device RNG on both sides; max_steps bounds the run."""
+    n, b, q, steps = 6656, 256, 1, 3
+    a = torch.empty((n, n), dtype=torch.float64, device="cuda").T
+    rutv.gaussian_matrix_device(a, 11)
+    ah = np.asfortranarray(a.cpu().numpy())
+    t1, u1, v1 = rutv.factorize(ah, b=b, q=q, seed=9, max_steps=steps)
+    t2, u2, v2 = rutv.factorize(ah, b=b, q=q, seed=9, max_steps=steps, grid=(1, 2), grid_sim=True)
+    k = steps * b
+    d = np.sign(np.einsum("ij,ij->j", u2[:, :k], u1[:, :k]))
+    assert np.max(np.abs(np.diag(t2)[:k] - np.diag(t1)[:k]) / np.diag(t1)[:k]) < 1e-10
+    assert np.max(np.abs(u2[:, :k] - u1[:, :k] * d)) < 1e-9 and np.max(np.abs(v2[:, :k] - v1[:, :k] * d)) < 1e-9
+    nf = np.linalg.norm(ah)
+    assert np.linalg.norm(ah - u2 @ t2 @ v2.T) / nf < 1e-13
+
+
 def test_grid_no_uv_same_t():
     n, b, q = 260, 32, 1
     a = oracle.gaussian_matrix(n, n, 8)
