@@ -64,6 +64,30 @@ METRIC = "randUTV FP64 effective GFLOP/s & time at 1/2/4/8 B200; % of FP64 TC pe
 DEFAULT_CONFIG = 5
 
 
+# The contract is ONE JSON line on stdout.  Native libraries (NCCL prints its version banner
+# with NCCL_DEBUG=VERSION/INFO) write to file descriptor 1 directly, so main() points fd 1 at
+# stderr for the whole run and emit() writes the result line to the saved stdout.
+_REAL_STDOUT = None
+
+
+def capture_stdout():
+    global _REAL_STDOUT
+    if _REAL_STDOUT is None:
+        sys.stdout.flush()
+        _REAL_STDOUT = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _REAL_STDOUT is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        sys.stdout.flush()
+        os.write(_REAL_STDOUT, data)
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -283,7 +307,7 @@ def run_reference(args):
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -335,6 +359,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    capture_stdout()
     args.warmup = max(args.warmup, 0)
     cfgd = CONFIGS[args.config]
     args.n = cfgd["n"] if args.n is None else args.n
@@ -506,7 +531,7 @@ def main():
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -630,7 +655,7 @@ def run_sharded(args, torch, dist, rutv, world, rank, local, dev, F):
                          "step_frac_of_peak": round(value / 1e3 / world / DMMA_PEAK_TFLOPS, 4)},
             "cpu_baseline": None,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -24,11 +24,15 @@ import oracle, paper_2104_05782_b200 as rutv
 from tests._util import cm_cuda, cm_empty, to_np
 out = []
 for s, w, kind in ((2000, 128, "gauss"), (4000, 128, "gauss"), (700, 100, "gauss"), (130, 48, "gauss"), (64, 64, "gauss"),
-                   (9000, 64, "gauss"), (300, 64, "graded"), (96, 32, "tri")):
+                   (9000, 64, "gauss"), (300, 64, "graded"), (96, 32, "tri"), (500, 48, "tiny"), (500, 48, "huge")):
     if kind == "gauss":
         y = oracle.gaussian_matrix(s, w, 7)
     elif kind == "graded":  # columns scaled over 12 decades: the Gram matrix of a micro-panel is ill-conditioned
         y = oracle.gaussian_matrix(s, w, 8) * np.logspace(0, -12, w)[None, :]
+    elif kind == "tiny":    # X'X ~ 1e-282: outside the pivot range the Gram path accepts -> column loop
+        y = oracle.gaussian_matrix(s, w, 9) * 1e-142  # (the reference's own sum of squares is still normal)
+    elif kind == "huge":    # X'X ~ 1e284
+        y = oracle.gaussian_matrix(s, w, 9) * 1e141
     else:                   # already triangular: tau = 0 reflectors (LU pivot 0 -> column loop)
         y = np.triu(np.ones((s, w)))
     p = min(s, w)
@@ -56,4 +60,4 @@ def test_cq_micro_panels_match_oracle(mode):
         if r["kind"] == "tri":
             assert r["r"] == 0.0 and r["v"] == 0.0 and r["tau"] == 0.0, r  # returned bit-equal, tau = 0
         else:
-            assert r["r"] < 1e-12 and r["v"] < 1e-11 and r["tau"] < 1e-12 and r["twy"] < 1e-10, r
+            assert r["r"] < 1e-12 and r["v"] < 1e-11 and r["tau"] < 1e-12 and r["twy"] < 1e-10, r  # NaN fails too

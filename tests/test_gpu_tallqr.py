@@ -76,6 +76,13 @@ def test_tall_panel_unsafe_subpanels_fall_back():
     assert np.max(np.abs(tau[:128] - tau_ref)) <= 1e-13
 
 
+@pytest.mark.parametrize("scale", [1e-142, 1e141])
+def test_tall_panel_extreme_scaling(scale):
+    # Y'Y ~ 1e-282 / 1e284, close to the ends of the double range (where the reference's own
+    # sums of squares are still normal numbers)
+    _check(oracle.gaussian_matrix(6300, 40, 23) * scale, 1e-13, 1e-13, 1e-13)  # R relative to max |R|
+
+
 def test_tall_panel_triangular_head_keeps_tau_zero_convention():
     s, w = 6200, 64
     y = np.triu(np.ones((s, w)))  # already upper triangular: every reflector is tau = 0
