@@ -252,6 +252,10 @@ void rutv_b200_set_stream(uint64_t stream);
 int rutv_b200_gemm_async(double alpha, int ta, const double* A, int64_t ar, int64_t ac, int64_t lda, int tb,
                          const double* B, int64_t br, int64_t bc, int64_t ldb, double beta, double* C, int64_t m,
                          int64_t n, int64_t ldc, rutv_status* st);
+/* hqr_inplace (householder.cpp:48-67).  Panels of >= 6144 rows (RUTV_CHOLQR_MIN_ROWS) factor their
+ * 128-column sub-panels by Cholesky-QR2 + Householder reconstruction and read one safety flag per
+ * sub-panel back from the device, i.e. synchronise the host with the current stream that many
+ * times before returning; shorter panels stay fully asynchronous. */
 int rutv_b200_hqr_async(double* A, int64_t m, int64_t n, int64_t lda, double* tau, rutv_status* st);
 /* W (unit-lower), Twy and M = W Twy' of a packed QR (householder.cpp:37-44, 76-97). */
 int rutv_b200_form_wy(const double* qr, int64_t s, int64_t ldq, const double* tau, int64_t p, double* W,
