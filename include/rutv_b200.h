@@ -252,7 +252,7 @@ void rutv_b200_set_stream(uint64_t stream);
 int rutv_b200_gemm_async(double alpha, int ta, const double* A, int64_t ar, int64_t ac, int64_t lda, int tb,
                          const double* B, int64_t br, int64_t bc, int64_t ldb, double beta, double* C, int64_t m,
                          int64_t n, int64_t ldc, rutv_status* st);
-/* hqr_inplace (householder.cpp:48-67).  Panels of >= 6144 rows (RUTV_CHOLQR_MIN_ROWS) factor their
+/* hqr_inplace (householder.cpp:48-67).  Panels of >= 4608 rows (RUTV_CHOLQR_MIN_ROWS) factor their
  * 128-column sub-panels by Cholesky-QR2 + Householder reconstruction and read one safety flag per
  * sub-panel back from the device, i.e. synchronise the host with the current stream that many
  * times before returning; shorter panels stay fully asynchronous. */

@@ -333,6 +333,33 @@ void form_t(cudaStream_t stream, const double* gram, int64_t ldg, const double* 
         form_t_small(stream, gram, ldg, tau, p, t, ldt);
         return;
     }
+    // p > 128: 128-column diagonal blocks by the blocked inversion (form_t_small), block column J
+    // by the two-block composition of compact-WY factors on the DMMA GEMM,
+    //     T(0:j0, J) = -T(0:j0, 0:j0) (G(0:j0, J) T_JJ)
+    // (the reference recurrence householder.cpp:84-95 a block at a time).  X' = T_JJ' G(0:j0, J)'
+    // is staged in T's own block below the diagonal, which is zeroed afterwards.  The single-CTA
+    // kernels below (RUTV_FORMT=legacy) take 5.1 ms at p = 512 -- on the critical chain of every
+    // late step, 2.3 % of config 5's kernel time (profiles/r02_launches_c5_full_b.json).
+    static const bool legacy = [] {
+        const char* e = std::getenv("RUTV_FORMT");
+        return e && std::string(e) == "legacy";
+    }();
+    if (!rd_only && !legacy && t != gram) {
+        const int64_t nbk = 128;
+        for (int64_t j0 = 0; j0 < p; j0 += nbk) {
+            const int64_t jb = std::min(nbk, p - j0);
+            double* tjj = t + j0 + j0 * ldt;
+            form_t_small(stream, gram + j0 + j0 * ldg, ldg, tau + j0, jb, tjj, ldt);
+            if (j0 == 0) continue;
+            const DView Tjj(jb, jb, ldt, tjj), Gj(j0, jb, ldg, const_cast<double*>(gram) + j0 * ldg);
+            const DView Xt(jb, j0, ldt, t + j0), T11(j0, j0, ldt, t), Tj(j0, jb, ldt, t + j0 * ldt);
+            gemm(stream, 1.0, Op::T, Tjj, Op::T, Gj, 0.0, Xt, nullptr, 0);
+            gemm(stream, -1.0, Op::N, T11, Op::T, Xt, 0.0, Tj, nullptr, 0);
+            RUTV_CUDA(cudaMemset2DAsync(t + j0, static_cast<size_t>(ldt) * sizeof(double), 0,
+                                        static_cast<size_t>(jb) * sizeof(double), static_cast<size_t>(j0), stream));
+        }
+        return;
+    }
     if (p <= 256) {
         static int rcap = 0;
         once_per_device(reinterpret_cast<const void*>(form_t_rd_kernel), [] {

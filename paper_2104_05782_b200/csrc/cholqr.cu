@@ -49,6 +49,7 @@
 #include <cstring>
 
 #include "rutv_common.cuh"
+#include "small_chains.cuh"
 
 namespace rutv {
 
@@ -243,14 +244,36 @@ __global__ void __launch_bounds__(kST) cqr_chol_kernel(const double* __restrict_
     CQR_CLK(base);
     load_square(A, p, P, [&](int i, int k) { return g[i + static_cast<int64_t>(k) * ldg]; });
     __syncthreads();
+    // Pass 2 factors G = Q1'Q1 = I + E.  With |E| <= 1e-11 the series R2 = I + U1, R2^-1 = I - U1,
+    // U1 = striu(E) + diag(E) / 2, is exact to ||U1||^2 <= (128 * 1e-11)^2 ~ 1.6e-18: no factorization
+    // (the four 32-column block steps are ~100 K cycles of this kernel's ~145 K).
+    bool series = false;
     if (check_orth) {
-        bool bad_orth = false;
-        for_rect(0, p, 0, p, [&](int i, int k) { bad_orth |= fabs(A(i, k) - (i == k ? 1.0 : 0.0)) > 0.1; });
+        bool bad_orth = false, big = false;
+        for_rect(0, p, 0, p, [&](int i, int k) {
+            const double e = fabs(A(i, k) - (i == k ? 1.0 : 0.0));
+            bad_orth |= e > 0.1;
+            big |= !(e <= 1e-11);
+        });
         if (__any_sync(kFull, bad_orth) && lane == 0) atomicOr(flag, 16);
+        series = __syncthreads_or(big ? 1 : 0) == 0;
+        if (series) {
+            // upper triangle: R2; strictly lower: R2^-1 transposed (the layout xinv() reads)
+            for_rect(0, P, 0, P, [&](int i, int k) {
+                if (i < k) {
+                    A(k, i) = -A(i, k);
+                } else if (i == k) {
+                    const double d = 1.0 + 0.5 * (A(k, k) - 1.0);
+                    A(k, k) = d;
+                    dinv[k] = 1.0 / d;
+                }
+            });
+            __syncthreads();
+        }
     }
     CQR_CLK(base + 1);
     bool bad = false;
-    for (int J = 0; J < NB; ++J) {
+    for (int J = 0; J < (series ? 0 : NB); ++J) {
         const int j0 = 32 * J;
         if (warp == 0) {
             // diagonal block in registers: lane k holds column j0 + k; row c of
@@ -410,38 +433,34 @@ __global__ void __launch_bounds__(kST) cqr_lu_kernel(const double* __restrict__ 
             double v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = A(j0 + i, j0 + lane);
-            // Branch-free chain (a small pivot only sets the flag); the next
-            // pivot's multiplier and update go first, the rest of the column's
-            // broadcasts after it.
-            double myinv = 1.0;
+            __syncwarp();
+            // Branch-free chain (a small pivot only sets the flag) on a shifting register window,
+            // one shared-memory round trip per step (small_chains.cuh, warp_lu16): lane c
+            // publishes its pivot and the raw column below it, every lane reads them back, scales
+            // by the reciprocal itself and updates with ONE fma per entry; row c of the packed
+            // factors goes straight to A.  ~330 cycles per column (a shuffle per multiplier: 800).
             bool brk = false;
-            double piv = __shfl_sync(kFull, v[0], 0);
-#pragma unroll
+            const uint32_t colb = smem_u32(rowb);
+#pragma unroll 1
             for (int c = 0; c < 32; ++c) {
+                const uint32_t col = colb + 8u * static_cast<uint32_t>((c & 1) * 32);
+                const double u0 = v[0];  // U(c, lane) for lane >= c, L(c, lane) for lane < c
+                if (lane == c) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) sts_v2f64(col + 8u * i, v[i], v[i + 1]);
+                }
+                __syncwarp();
+                const double piv = lds_f64(col);
+                const double inv = chain_rcp(piv);
+                const double a = lane > c ? -(u0 * inv) : (lane == c ? inv - 1.0 : 0.0);
+#pragma unroll
+                for (int i = 1; i < 32; ++i) v[i - 1] = __fma_rn(lds_f64(col + 8u * i), a, v[i]);
+                v[31] = 0.0;
                 brk |= !(fabs(piv) >= 0.25) || !isfinite(piv);
-                const double inv = __drcp_rn(piv);
-                myinv = lane == c ? inv : myinv;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (i > c && lane == c) v[i] *= inv;  // multipliers L(i, c)
-                if (c + 1 < 32) {
-                    const int n1 = c + 1 < 32 ? c + 1 : c;
-                    const double l1 = __shfl_sync(kFull, v[n1], c);
-                    if (lane > c) v[n1] = __fma_rn(-l1, v[c], v[n1]);
-                    piv = __shfl_sync(kFull, v[n1], n1);
-                }
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    if (i > c + 1) {
-                        const double li = __shfl_sync(kFull, v[i], c);
-                        if (lane > c) v[i] = __fma_rn(-li, v[c], v[i]);
-                    }
-                }
+                A(j0 + c, j0 + lane) = u0;
+                if (lane == c) dinv[j0 + c] = inv;
             }
-            dinv[j0 + lane] = myinv;
             bad |= brk;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) A(j0 + i, j0 + lane) = v[i];
             __syncwarp();
             double x[32];
             warp_upper_inv(A, j0, dinv, x);  // XD = U_JJ^{-1} (lane k: column k)
@@ -622,7 +641,7 @@ thread_local int* t_deferred_flag = nullptr;
 int64_t tall_min_rows() {
     static const int64_t v = [] {
         const char* e = std::getenv("RUTV_CHOLQR_MIN_ROWS");
-        return e ? std::atoll(e) : static_cast<int64_t>(6144);
+        return e ? std::atoll(e) : static_cast<int64_t>(4608);
     }();
     return v;
 }

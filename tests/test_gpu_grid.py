@@ -50,7 +50,7 @@ def test_grid_matches_single_gpu_device_rng():
 
 
 def test_grid_tall_panels_match_single_gpu():
-    """n above RUTV_CHOLQR_MIN_ROWS (6144): every rank factors the gathered sketch and the
+    """n above RUTV_CHOLQR_MIN_ROWS (4608): every rank factors the gathered sketch and the
     diagonal owner the panel through the Cholesky-QR2 sub-panels, each reading its safety flag
     back with a host synchronisation of its own critical stream -- inside the rank threads of
     the in-process grid.  Device RNG on both sides; max_steps bounds the run."""

@@ -1,4 +1,4 @@
-"""Tall panels (rows >= RUTV_CHOLQR_MIN_ROWS, default 6144) factor their <= 128-column
+"""Tall panels (rows >= RUTV_CHOLQR_MIN_ROWS, default 4608) factor their <= 128-column
 sub-panels by Cholesky-QR2 + Householder reconstruction (cholqr.cu, qr_cluster.cu
 hqr_panel) and must reproduce the reference's hqr_inplace (householder.cpp:48-67):
 packed R / V and tau against the oracle, on a well-conditioned panel (fast path
