@@ -134,10 +134,10 @@ __device__ __forceinline__ void dmma(double* c, double a0, double a1, double b) 
 
 // Reflector entry V(li, c) of the micro-panel starting at global column j0:
 // unit lower trapezoidal (1 on the diagonal, 0 above, 0 for c >= kb).
-__device__ __forceinline__ double vent(const double* chunk, int LD, int li, int rc, int gi, int j0, int c, int kb) {
+__device__ __forceinline__ double vent(uint32_t chunk_a, int LD, int li, int rc, int gi, int j0, int c, int kb) {
     if (li >= rc || c >= kb) return 0.0;
     const int j = j0 + c;
-    if (gi > j) return chunk[static_cast<size_t>(j) * LD + li];
+    if (gi > j) return lds_f64(chunk_a + 8u * static_cast<uint32_t>(j * LD + li));
     return gi == j ? 1.0 : 0.0;
 }
 
@@ -160,6 +160,22 @@ __global__ void __launch_bounds__(kT, 1)
     const int r_beg = rank * R;
     const int rc = max(0, min(s, r_beg + R) - r_beg);
     const int nwact = max(1, min(kWarps, (rc + 31) >> 5));  // warps owning rows (warp 0 always)
+
+    // Every shared-memory region by its 32-bit shared-window address, derived from ONE opaque
+    // register (sm_a) plus the carve offsets.  A generic pointer access -- or a rematerialised
+    // smem_u32() -- costs an S2R SR_CgaCtaId + LEA in a cluster kernel, and this kernel's phases
+    // are single-warp latency chains: ptxas put those reads INSIDE the one-warp Cholesky / LU loops
+    // (5.2 K -> 7.8 K cycles per chain) until the addresses became opaque to it.
+    uint32_t sm_a;
+    asm volatile("mov.u32 %0, %1;" : "=r"(sm_a) : "r"(smem_u32(sm)));
+    auto addr = [&](const void* q) {
+        return sm_a + static_cast<uint32_t>(reinterpret_cast<const char*>(q) - reinterpret_cast<const char*>(sm));
+    };
+    const uint32_t msg_a = addr(S.msg);
+    const uint32_t part_a = addr(S.part), hsend_a = addr(S.hsend), chunk_a = sm_a;
+    const uint32_t bar0 = addr(S.bar);  // mbarrier b at bar0 + 8 b
+    const uint32_t rsb_a = addr(S.rsb), gin2_a = addr(S.gin2), zg_a = addr(S.zg), tmat_a = addr(S.tmat);
+    const uint32_t taus_a = addr(S.taus), cqb_a = addr(S.cq);
 
     for (int idx = tid; idx < w * rc; idx += kT) {
         const int c = idx / rc, i = idx - c * rc;
@@ -197,20 +213,16 @@ __global__ void __launch_bounds__(kT, 1)
         // completed wait.  A message may land before its barrier is armed: the phase only
         // completes with the arming thread's own arrival.
         if (cq_mode) {
-            mbar_arm(&S.bar[4], hop1_bytes);
-            mbar_arm(&S.bar[5], hop2_bytes);
+            mbar_arm_a(bar0 + 8u * 4, hop1_bytes);
+            mbar_arm_a(bar0 + 8u * 5, hop2_bytes);
         }
         const int f = (0 + min(KB, w) < w && p > 0) ? 0 : next_phase_j0(0);
         if (nphase > 0 && f >= 0) {
-            mbar_arm(&S.bar[2], rs_bytes(f));
-            mbar_arm(&S.bar[3], ag_bytes(f));
+            mbar_arm_a(bar0 + 8u * 2, rs_bytes(f));
+            mbar_arm_a(bar0 + 8u * 3, ag_bytes(f));
         }
     }
     cluster.sync();  // every CTA live, barriers initialised, before any remote traffic
-
-    const uint32_t msg_a = smem_u32(S.msg);
-    const uint32_t part_a = smem_u32(S.part), hsend_a = smem_u32(S.hsend), chunk_a = smem_u32(S.chunk);
-    const uint32_t bar0 = smem_u32(S.bar);  // mbarrier b at bar0 + 8 b
 
     // Reduce the 16 per-thread partial dots over the row-owning warps and
     // all-gather them, with the head row of column jn, to every CTA's message
@@ -301,25 +313,26 @@ __global__ void __launch_bounds__(kT, 1)
         const bool gt = trace && tid == 0 && rank == 0 && (j0 >> 4) < 8 && barid == 4;
         if (gt) trace[72 * 8 + (j0 >> 4) * 16 + 12] = clock64();
         // 16 warp partials in 8 slots: warps 0-7 store, warps 8-15 add
-        double* slot = S.part + (warp & 7) * kCqMat;
+        const uint32_t slot = part_a + 8u * static_cast<uint32_t>((warp & 7) * kCqMat);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
             if ((warp >> 3) == half) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const int idx = (g + (r >= 2 ? 8 : 0)) * KB + 2 * t4 + (r & 1);
+                    const uint32_t sa = slot + 8u * static_cast<uint32_t>(idx);
                     if (half == 0) {
-                        slot[idx] = c0[r];
-                        slot[idx + 8] = c1[r];
+                        sts_f64(sa, c0[r]);
+                        sts_f64(sa + 64u, c1[r]);
                     } else {
-                        slot[idx] += c0[r];
-                        slot[idx + 8] += c1[r];
+                        sts_f64(sa, lds_f64(sa) + c0[r]);
+                        sts_f64(sa + 64u, lds_f64(sa + 64u) + c1[r]);
                     }
                 }
             }
             __syncthreads();
         }
-        const uint32_t stg = smem_u32(S.cq) + kStg + (barid == 5 ? 8u * kNG : 0u);
+        const uint32_t stg = cqb_a + kStg + (barid == 5 ? 8u * kNG : 0u);
         if (gt) trace[72 * 8 + (j0 >> 4) * 16 + 13] = clock64();
         if (tid < kNG) {
             double v = 0.0;
@@ -333,7 +346,7 @@ __global__ void __launch_bounds__(kT, 1)
         // 68 pairs x CS destinations spread over all threads (16-byte remote stores: the CTA's
         // remote-store rate bounds this exchange; a bulk DSMEM copy per destination was
         // measured slower -- ~1.2 K cycles to issue behind a proxy fence)
-        const uint32_t inbox_a = smem_u32(inbox) + 8u * static_cast<uint32_t>(rank * kNG);
+        const uint32_t inbox_a = addr(inbox) + 8u * static_cast<uint32_t>(rank * kNG);
         for (int idx = tid; idx < (kNG / 2) * CS; idx += kT) {
             const int dst = idx / (kNG / 2), pr = idx - dst * (kNG / 2);
             double a, b;
@@ -353,13 +366,15 @@ __global__ void __launch_bounds__(kT, 1)
             const int li = tid + kT * m;
 #pragma unroll
             for (int k = 0; k < KB; ++k)
-                x[m][k] = (li < rc && k < kt) ? S.chunk[static_cast<size_t>(j0 + k) * LD + li] : 0.0;
+                x[m][k] = (li < rc && k < kt) ? lds_f64(chunk_a + 8u * static_cast<uint32_t>((j0 + k) * LD + li)) : 0.0;
         }
         // ---- CQ fast path for a full micro-panel (see the header); hh = the column loop runs
         bool hh = true;
         if (cq_mode && kb == KB && kt == KB && s - j0 >= 2 * KB) {
             const int lo = min(rc, max(0, j0 - r_beg));  // local rows with gi >= j0
-            const uint32_t cq_a = smem_u32(S.cq), tmat_a = smem_u32(S.tmat);
+            const uint32_t cq_a = cqb_a, scr_a = part_a;
+            int lane_o;  // likewise the lane index (S2R SR_TID.X in the loops otherwise)
+            asm volatile("mov.s32 %0, %1;" : "=r"(lane_o) : "r"(lane));
             int pe_i = 0, pe_k = 0;
             if (tid < kNG) packed_index(pe_i, pe_k);
             const bool force1 = cq_mode == 3 && ((j0 >> 4) & 1), force2 = cq_mode == 2 && ((j0 >> 4) & 1);
@@ -370,15 +385,15 @@ __global__ void __launch_bounds__(kT, 1)
             // -- pass 1: G = X'X, R1 = chol(G)
             gram_send(j0, lo, S.rsb, 4);
             CQT(1);
-            mbar_wait(&S.bar[4], (phbits >> 2) & 1u);
+            mbar_wait_a(bar0 + 8u * 4, (phbits >> 2) & 1u);
             phbits ^= 4u;
             CQT(2);
-            if (tid == 0) mbar_arm(&S.bar[4], hop1_bytes);
+            if (tid == 0) mbar_arm_a(bar0 + 8u * 4, hop1_bytes);
             if (tid < kNG) {
                 double v = 0.0;
-                for (int src = 0; src < CS; ++src) v += S.rsb[src * kNG + tid];
-                S.tmat[pe_i * KB + pe_k] = v;
-                S.tmat[pe_k * KB + pe_i] = v;
+                for (int src = 0; src < CS; ++src) v += lds_f64(rsb_a + 8u * static_cast<uint32_t>(src * kNG + tid));
+                sts_f64(tmat_a + 8u * static_cast<uint32_t>(pe_i * KB + pe_k), v);
+                sts_f64(tmat_a + 8u * static_cast<uint32_t>(pe_k * KB + pe_i), v);
             }
             __syncthreads();
             CQT(3);
@@ -386,9 +401,9 @@ __global__ void __launch_bounds__(kT, 1)
                 const int kk = lane & (KB - 1);
                 double v[KB];
 #pragma unroll
-                for (int i = 0; i < KB; ++i) v[i] = S.tmat[i * KB + kk];
+                for (int i = 0; i < KB; ++i) v[i] = lds_f64(tmat_a + 8u * static_cast<uint32_t>(i * KB + kk));
                 double mn, mx;
-                const bool brk = warp_chol16(v, cq_a + kRmat, cq_a + kRdinv, part_a, mn, mx, lane);
+                const bool brk = warp_chol16(v, cq_a + kRmat, cq_a + kRdinv, scr_a, mn, mx, lane_o);
                 if (lane == 0) sts_i32(cq_a + kFlag, (brk || !(mn > 1e-3 * mx) || force1) ? 1 : 0);
             }
             __syncthreads();
@@ -430,17 +445,17 @@ __global__ void __launch_bounds__(kT, 1)
                     }
                 }
                 CQT(6);
-                mbar_wait(&S.bar[5], (phbits >> 3) & 1u);
+                mbar_wait_a(bar0 + 8u * 5, (phbits >> 3) & 1u);
                 CQT(7);
                 phbits ^= 8u;
-                if (tid == 0) mbar_arm(&S.bar[5], hop2_bytes);
+                if (tid == 0) mbar_arm_a(bar0 + 8u * 5, hop2_bytes);
                 bool bad = false;
                 if (tid < kNG) {
                     double v = 0.0;
-                    for (int src = 0; src < CS; ++src) v += S.gin2[src * kNG + tid];
+                    for (int src = 0; src < CS; ++src) v += lds_f64(gin2_a + 8u * static_cast<uint32_t>(src * kNG + tid));
                     const double e = v - (pe_i == pe_k ? 1.0 : 0.0);
-                    S.tmat[pe_i * KB + pe_k] = e;
-                    S.tmat[pe_k * KB + pe_i] = e;
+                    sts_f64(tmat_a + 8u * static_cast<uint32_t>(pe_i * KB + pe_k), e);
+                    sts_f64(tmat_a + 8u * static_cast<uint32_t>(pe_k * KB + pe_i), e);
                     bad = !(fabs(e) <= 1e-9);
                 }
                 bool redo = __syncthreads_or(bad || force2) != 0;
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(kT, 1)
                         for (int i = 0; i < KB; ++i) v[i] = lds_f64(cq_a + kLumat + 8u * (i * KB + kk));
                         __syncwarp();
                         // tau = diag(U) lands in S.taus (the block phase's T recurrence reads it)
-                        const bool brk = warp_lu16(v, cq_a + kLumat, cq_a + kUdinv, smem_u32(S.taus), part_a, lane);
+                        const bool brk = warp_lu16(v, cq_a + kLumat, cq_a + kUdinv, taus_a, scr_a, lane_o);
                         const bool any = __any_sync(kFull, brk);
                         if (lane == 0) sts_i32(cq_a + kFlag + 4u, any ? 1 : 0);
                     }
@@ -481,7 +496,23 @@ __global__ void __launch_bounds__(kT, 1)
                     redo = lds_i32(cq_a + kFlag + 4u) != 0;
                 }
                 if (!redo) {
-                    if (rank == 0 && tid < KB) tau[j0 + tid] = S.taus[tid];
+                    if (rank == 0 && tid < KB) tau[j0 + tid] = lds_f64(taus_a + 8u * tid);
+                    // T of the block reflector from the reconstruction itself: U = T V1' with V1 = L,
+                    // so row i of T solves t_i L' = u_i (one warp, beside the row finalisation);
+                    // the block phase then needs neither V'V nor the form_wy_t recurrence.
+                    if (warp == kWarps - 1 && lane < KB) {
+                        double trow[KB];
+#pragma unroll
+                        for (int k = 0; k < KB; ++k) {
+                            double acc = k >= lane ? lds_f64(cq_a + kLumat + 8u * (lane * KB + k)) : 0.0;
+#pragma unroll
+                            for (int m2 = 0; m2 < k; ++m2)
+                                acc = __fma_rn(-trow[m2], lds_f64(cq_a + kLumat + 8u * (k * KB + m2)), acc);
+                            trow[k] = acc;
+                        }
+#pragma unroll
+                        for (int k = 0; k < KB; ++k) sts_f64(cq_a + kQ1in + 8u * (lane * KB + k), trow[k]);
+                    }
                     // -- V = [L; -Q(below) U^-1], R into the head rows; retire the micro-panel
 #pragma unroll
                     for (int m = 0; m < MR; ++m) {
@@ -544,8 +575,8 @@ __global__ void __launch_bounds__(kT, 1)
         // in every warp of the cluster), lane k forming w_k.
         if (hh && warp < nwact) {
             if (tid == 0) {
-                mbar_arm(&S.bar[0], col_bytes);
-                if (kb > 1) mbar_arm(&S.bar[1], col_bytes);
+                mbar_arm_a(bar0 + 8u * 0, col_bytes);
+                if (kb > 1) mbar_arm_a(bar0 + 8u * 1, col_bytes);
             }
             {  // partials of column j0: x_j0' x_{j0+k} over rows > j0, head row j0
                 double vals[KB];
@@ -569,7 +600,7 @@ __global__ void __launch_bounds__(kT, 1)
                 const int j = j0 + c, par = j & 1;
                 const bool tr = trace && tid == 0 && rank == 0 && j < 64;
                 if (tr) trace[j * 8 + 0] = clock64();
-                mbar_wait(&S.bar[par], ((phbits >> par) + static_cast<unsigned>(c >> 1)) & 1u);
+                mbar_wait_a(bar0 + 8u * par, ((phbits >> par) + static_cast<unsigned>(c >> 1)) & 1u);
                 if (tr) trace[j * 8 + 1] = clock64();
                 double tsum;
                 {
@@ -665,9 +696,9 @@ __global__ void __launch_bounds__(kT, 1)
                     x[m][KB - 1] = 0.0;
                 }
                 if (tid == 0) {  // off the critical chain: re-arm slot par, record tau
-                    if (c + 2 < kb) mbar_arm(&S.bar[par], col_bytes);
+                    if (c + 2 < kb) mbar_arm_a(bar0 + 8u * par, col_bytes);
                     if (rank == 0) tau[j] = tj;
-                    S.taus[c] = tj;
+                    sts_f64(taus_a + 8u * static_cast<uint32_t>(c), tj);
                 }
                 if (tr) trace[j * 8 + 3] = clock64();
                 if (nxt) {
@@ -691,34 +722,36 @@ __global__ void __launch_bounds__(kT, 1)
             if (hh && li < rc) {
 #pragma unroll
                 for (int k = 0; k < KB; ++k)
-                    if (k < kt - kb) S.chunk[static_cast<size_t>(j0 + kb + k) * LD + li] = x[m][k];
+                    if (k < kt - kb) sts_f64(chunk_a + 8u * static_cast<uint32_t>((j0 + kb + k) * LD + li), x[m][k]);
             }
         }
         __syncthreads();
         if (j0 + kt >= w || (ablate & 1)) continue;
 
         const int tph = phase;
+        const bool have_t = !hh;  // the micro-panel took the CQ path: T sits in the CQ scratch
         if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 0] = clock64();
         // ---- block phase: A_t <- A_t - V T' (V' A_t), A_t = columns [j0 + kt, w)
         const int nrest = w - j0 - kt, ncol = KB + nrest;
         const int lo = min(rc, max(0, j0 - r_beg));  // local rows with gi >= j0
         const int nk4 = (rc - lo + 3) >> 2;
         {
-            // P = V'[V | A_t] over my rows: M = 16 (c), N = ncol (tiles of 8), K = rows
-            const int nt = (ncol + 7) >> 3;
-            const int ksplit = max(1, kWarps / nt);
+            // P = V'[V | A_t] over my rows: M = 16 (c), N = ncol (tiles of 8), K = rows; after a CQ
+            // micro-panel T is already known (have_t): the two tiles of V'V are skipped
+            const int tl0 = have_t ? 2 : 0, nt = ((ncol + 7) >> 3) - tl0;
+            const int ksplit = max(1, kWarps / (nt + tl0));  // [ksplit][16][ncol] fits `part` (part_elems)
             for (int u = warp; u < nt * ksplit; u += kWarps) {
-                const int tile = u % nt, ks = u / nt;
+                const int tile = tl0 + u % nt, ks = u / nt;
                 const int kb0 = (ks * nk4) / ksplit, kb1 = ((ks + 1) * nk4) / ksplit;
                 const int q = tile * 8 + g;  // my B column
                 double acc[4] = {0.0, 0.0, 0.0, 0.0}, acc2[4] = {0.0, 0.0, 0.0, 0.0};
                 auto slow = [&](int k4) {  // rows in the unit-triangle zone or past rc
                     const int li = lo + 4 * k4 + t4, gi = r_beg + li;
-                    const double a0 = vent(S.chunk, LD, li, rc, gi, j0, g, kb);
-                    const double a1 = vent(S.chunk, LD, li, rc, gi, j0, g + 8, kb);
+                    const double a0 = vent(chunk_a, LD, li, rc, gi, j0, g, kb);
+                    const double a1 = vent(chunk_a, LD, li, rc, gi, j0, g + 8, kb);
                     double b;
-                    if (q < KB) b = vent(S.chunk, LD, li, rc, gi, j0, q, kb);
-                    else if (q < ncol && li < rc) b = S.chunk[static_cast<size_t>(j0 + kt + q - KB) * LD + li];
+                    if (q < KB) b = vent(chunk_a, LD, li, rc, gi, j0, q, kb);
+                    else if (q < ncol && li < rc) b = lds_f64(chunk_a + 8u * static_cast<uint32_t>((j0 + kt + q - KB) * LD + li));
                     else b = 0.0;
                     dmma(acc, a0, a1, b);
                 };
@@ -729,7 +762,7 @@ __global__ void __launch_bounds__(kT, 1)
                 const int kfull = max(kspec, min(kb1, (rc - lo) >> 2));
                 const bool za0 = g >= kb, za1 = g + 8 >= kb, zb = q >= ncol || (q < KB && q >= kb);
                 // masked operands read a valid clamped column (column j0) and are zeroed by select
-                const uint32_t cbase = smem_u32(S.chunk) + 8u * static_cast<uint32_t>(lo + t4);
+                const uint32_t cbase = chunk_a + 8u * static_cast<uint32_t>(lo + t4);
                 const uint32_t pa0 = cbase + 8u * static_cast<uint32_t>((za0 ? j0 : j0 + g) * LD);
                 const uint32_t pa1 = cbase + 8u * static_cast<uint32_t>((za1 ? j0 : j0 + g + 8) * LD);
                 const uint32_t pb =
@@ -749,7 +782,7 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const int row = g + (r >= 2 ? 8 : 0), col = tile * 8 + 2 * t4 + (r & 1);
-                    if (col < ncol) S.part[(static_cast<size_t>(ks) * KB + row) * ncol + col] = acc[r];
+                    if (col < ncol) sts_f64(part_a + 8u * static_cast<uint32_t>((ks * KB + row) * ncol + col), acc[r]);
                 }
             }
             __syncthreads();
@@ -759,59 +792,60 @@ __global__ void __launch_bounds__(kT, 1)
             for (int e = tid; e < KB * ncol; e += kT) {
                 const int row = e / ncol, col = e - row * ncol;
                 double v = 0.0;
-                for (int ks = 0; ks < ksplit; ++ks) v += S.part[(static_cast<size_t>(ks) * KB + row) * ncol + col];
+                if (col >= 8 * tl0)
+                    for (int ks = 0; ks < ksplit; ++ks) v += lds_f64(part_a + 8u * static_cast<uint32_t>((ks * KB + row) * ncol + col));
                 const int o = col / ns;
                 const uint32_t off =
-                    smem_u32(S.rsb + (static_cast<size_t>(rank) * KB + row) * ns + (col - o * ns));
+                    rsb_a + 8u * static_cast<uint32_t>((rank * KB + row) * ns + (col - o * ns));
                 st_async_f64(mapa_u32(off, o), v, mapa_u32(bar0 + 16, o));
             }
             // owner: sum the CS partial slices in rank order and broadcast
-            mbar_wait(&S.bar[2], static_cast<uint32_t>(phase & 1));
+            mbar_wait_a(bar0 + 8u * 2, static_cast<uint32_t>(phase & 1));
     if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 2] = clock64();
             const int nxt = next_phase_j0(j0);
-            if (tid == 0 && nxt >= 0) mbar_arm(&S.bar[2], rs_bytes(nxt));
+            if (tid == 0 && nxt >= 0) mbar_arm_a(bar0 + 8u * 2, rs_bytes(nxt));
             const int mine = max(0, min(ncol, (rank + 1) * ns) - rank * ns);
             for (int e = tid; e < KB * mine; e += kT) {
                 const int row = e / mine, qq = e - row * mine;
                 double v = 0.0;
-                for (int src = 0; src < CS; ++src) v += S.rsb[(static_cast<size_t>(src) * KB + row) * ns + qq];
-                const uint32_t off = smem_u32(S.zg + static_cast<size_t>(row) * ncol + rank * ns + qq);
+                for (int src = 0; src < CS; ++src) v += lds_f64(rsb_a + 8u * static_cast<uint32_t>((src * KB + row) * ns + qq));
+                const uint32_t off = zg_a + 8u * static_cast<uint32_t>(row * ncol + rank * ns + qq);
                 for (int dst = 0; dst < CS; ++dst) st_async_f64(mapa_u32(off, dst), v, mapa_u32(bar0 + 24, dst));
             }
-            mbar_wait(&S.bar[3], static_cast<uint32_t>(phase & 1));
+            mbar_wait_a(bar0 + 8u * 3, static_cast<uint32_t>(phase & 1));
     if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 3] = clock64();
-            if (tid == 0 && nxt >= 0) mbar_arm(&S.bar[3], ag_bytes(nxt));
+            if (tid == 0 && nxt >= 0) mbar_arm_a(bar0 + 8u * 3, ag_bytes(nxt));
             ++phase;
         }
         // T (form_wy_t recurrence, householder.cpp:69-97): T(c,c) = tau_c,
         // T(0:c, c) = -tau_c T(0:c, 0:c) G(0:c, c), G = V'V = zg[:, 0:16]
-        if (warp == 0) {
+        if (warp == 0 && !have_t) {
             double trow[KB];
 #pragma unroll
             for (int c = 0; c < KB; ++c) {
-                const double tc = S.taus[c < kb ? c : 0];
+                const double tc = lds_f64(taus_a + 8u * static_cast<uint32_t>(c < kb ? c : 0));
                 double acc = 0.0;
 #pragma unroll
-                for (int q = 0; q < c; ++q) acc += trow[q] * S.zg[q * ncol + c];
+                for (int q = 0; q < c; ++q) acc += trow[q] * lds_f64(zg_a + 8u * static_cast<uint32_t>(q * ncol + c));
                 trow[c] = c >= kb ? 0.0 : (lane < c ? -tc * acc : (lane == c ? tc : 0.0));
             }
             if (lane < KB)
 #pragma unroll
-                for (int c = 0; c < KB; ++c) S.tmat[lane * KB + c] = trow[c];
+                for (int c = 0; c < KB; ++c) sts_f64(tmat_a + 8u * static_cast<uint32_t>(lane * KB + c), trow[c]);
         }
         __syncthreads();
         if (trace && tid == 0 && rank == 0 && tph < 8) trace[64 * 8 + tph * 8 + 4] = clock64();
-        // Y = -T' Z in place (Z = zg[:, 16:])
-        for (int k = tid; k < nrest; k += kT) {
-            double z[KB];
-#pragma unroll
-            for (int q = 0; q < KB; ++q) z[q] = S.zg[q * ncol + KB + k];
-#pragma unroll
-            for (int c = 0; c < KB; ++c) {
+        // Y = -T' Z (Z = zg[:, 16:]) into part[16][nrest], one entry per thread and pass
+        {
+            const uint32_t tsrc = have_t ? cqb_a + kQ1in : tmat_a;
+            const uint32_t zsrc = zg_a;
+            for (int e = tid; e < KB * nrest; e += kT) {
+                const int c = e / nrest, k = e - c * nrest;
                 double acc = 0.0;
-#pragma unroll
-                for (int q = 0; q <= c; ++q) acc += S.tmat[q * KB + c] * z[q];
-                S.zg[c * ncol + KB + k] = -acc;
+                for (int q = 0; q <= c; ++q)
+                    acc = __fma_rn(lds_f64(tsrc + 8u * static_cast<uint32_t>(q * KB + c)),
+                                   lds_f64(zsrc + 8u * static_cast<uint32_t>(q * ncol + KB + k)), acc);
+                sts_f64(part_a + 8u * static_cast<uint32_t>(e), -acc);
             }
         }
         __syncthreads();
@@ -830,12 +864,12 @@ __global__ void __launch_bounds__(kT, 1)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int li = r0 + g + 8 * h;
-                        av[ks][h] = ks < nk ? vent(S.chunk, LD, li, rc, r_beg + li, j0, 4 * ks + t4, kb) : 0.0;
+                        av[ks][h] = ks < nk ? vent(chunk_a, LD, li, rc, r_beg + li, j0, 4 * ks + t4, kb) : 0.0;
                     }
                 // two column tiles per iteration: both loaded before either is
                 // stored (a load after a store to the chunk cannot be hoisted),
                 // two independent DMMA chains
-                const uint32_t cb = smem_u32(S.chunk), zb0 = smem_u32(S.zg);
+                const uint32_t cb = chunk_a;
                 for (int tn = ng; tn < ntl; tn += 2 * ngr) {
                     double acc[2][4];
                     uint32_t ad[2][4];
@@ -860,8 +894,8 @@ __global__ void __launch_bounds__(kT, 1)
                             for (int h2 = 0; h2 < 2; ++h2) {
                                 const int yc = (h2 ? tn2 : tn) * 8 + g;
                                 const bool yok = yc < nrest;
-                                const double bv = lds_f64(
-                                    zb0 + 8u * static_cast<uint32_t>((4 * ks + t4) * ncol + KB + (yok ? yc : 0)));
+                                const double bv =
+                                    lds_f64(part_a + 8u * static_cast<uint32_t>((4 * ks + t4) * nrest + (yok ? yc : 0)));
                                 dmma(acc[h2], av[ks][0], av[ks][1], yok ? bv : 0.0);
                             }
                         }
