@@ -24,7 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
 # The device RNG restates the reference's no-contraction arithmetic
 # (proj/CMakeLists.txt:17-18 -ffp-contract=off) -> no FMA fusion there.
 PER_FILE = {"rng.cu": ["--fmad=false"]}
-SOURCES = ["gemm_f64.cu", "rng.cu", "aux_kernels.cu", "qr_cluster.cu", "qr_reg.cu", "cholqr.cu", "jacobi.cu", "randutv.cu", "rect.cu", "grouped.cu", "gen.cu", "capi.cu", "stream_api.cu", "io_metrics.cu", "runtime.cu", "step_api.cu", "dist.cu"]
+SOURCES = ["gemm_f64.cu", "rng.cu", "aux_kernels.cu", "qr_cluster.cu", "qr_reg.cu", "cholqr.cu", "jacobi.cu", "jacobi_blk.cu", "randutv.cu", "rect.cu", "grouped.cu", "gen.cu", "capi.cu", "stream_api.cu", "io_metrics.cu", "runtime.cu", "step_api.cu", "dist.cu"]
 
 
 def _digest() -> str:

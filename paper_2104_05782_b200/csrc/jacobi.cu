@@ -605,11 +605,24 @@ JCfg choose(int n, int count = 1) {
 }  // namespace
 
 // V spill (CS x n x (R | 1) <= n (n + 16)) + completion candidate
-int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) { return n * (n + 16) + n + 64; }
+int64_t svd_blk_work_elems(int64_t n);
+bool svd_blk_applicable(int nmax);
+void svd_batch_blk(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol, int max_sweeps);
+
+int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) {
+    return std::max<int64_t>(n * (n + 16) + n + 64, svd_blk_work_elems(n));
+}
 
 void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol,
                int max_sweeps) {
     if (count <= 0) return;
+    if (svd_blk_applicable(nmax)) {  // blocks up to 256 wide: the column-distributed kernel (jacobi_blk.cu)
+        svd_batch_blk(stream, d_descs, count, nmax, tol, max_sweeps);
+        complete_kernel<<<count, 256, 0, stream>>>(d_descs);
+        note_launch();
+        RUTV_CHECK_LAUNCH();
+        return;
+    }
     const JCfg c = choose(nmax, count);
     const int rs = use_rs(nmax, c.cs) ? 1 : 0;
     cudaLaunchConfig_t cfg = {};

@@ -1,0 +1,368 @@
+// jacobi_blk.cu -- batched one-sided Jacobi SVD with COLUMN-distributed blocks (n <= 256).
+//
+// Same algorithm contract as jacobi.cu (reference proj/src/jacobi_svd.cpp:39-148: one-sided
+// Jacobi on the columns of a square block, thresholds rel = max(tol, sqrt(n) eps) and
+// floor = 4 n eps ||A||_F, a sweep without rotations ends the iteration, max_sweeps ->
+// ConvergenceError with the worst remaining pair ratio, stable descending sort, U = b / sigma),
+// different data distribution.  jacobi.cu splits the ROWS of a block over the CTAs of a cluster,
+// so every pair's three dot products cross the cluster every round (one DSMEM exchange + two CTA
+// barriers per round, ~5 K cycles for n = 128).  Here the block's columns are cut into NB = 2 CS
+// column blocks of 16; a CTA holds TWO column blocks (32 whole columns of B and of V) in shared
+// memory and one WARP owns a pair: dots, decision and rotation are warp-local (shuffles only), a
+// round costs one CTA barrier, and the cluster only meets when the column blocks are re-paired:
+//   super-round sr of a sweep: CTA c takes the block pair rr_pair(NB, sr, c) of a round-robin
+//   tournament over the blocks; the first super-round rotates all 31 x 16 pairs of its 32
+//   columns, the others only the 16 x 16 cross pairs -- 31 + (NB - 2) 16 = N - 1 rounds per
+//   sweep, every column pair exactly once.
+// Between super-rounds the blocks live in a global master copy (the problem's work buffer, L2
+// resident): store both blocks, fence, cluster barrier, load the next two.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstdlib>
+#include <cstring>
+
+#include "rutv_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rutv {
+
+namespace {
+
+constexpr int kBT = 512;  // threads: 16 warps = the 16 pairs of a local round
+constexpr int kBW = 16;   // columns per block
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// round-robin pairing of N (even) players: round r in [0, N - 1), pair pi in [0, N / 2)
+__device__ __forceinline__ void rrp(int N, int r, int pi, int& p, int& q) {
+    auto pos = [&](int k) {
+        if (k == 0) return 0;
+        int v = k - 1 + r;
+        if (v >= N - 1) v -= N - 1;
+        return 1 + v;
+    };
+    const int x = pos(pi), y = pos(N - 1 - pi);
+    p = min(x, y);
+    q = max(x, y);
+}
+
+// jacobi_svd.cpp:60-85: skip tests and the rotation (c, s) of a pair from its three dots
+__device__ __forceinline__ bool jdecide(double al, double be, double ga, double rel, double floor_col, double& c,
+                                        double& s, double& ratio) {
+    const double np = sqrt(al), nq = sqrt(be);
+    const double zeta = (be - al) / (2.0 * ga);
+    ratio = -1.0;
+    if (np <= floor_col || nq <= floor_col) return false;
+    const double pq = np * nq;
+    ratio = fabs(ga) / pq;
+    if (fabs(ga) <= rel * pq) return false;
+    const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    c = rsqrt(1.0 + tt * tt);
+    s = c * tt;
+    return true;
+}
+
+template <int RPT>  // rows per lane: n <= 32 RPT
+__global__ void __launch_bounds__(kBT, 1)
+    jacobi_blk_kernel(const SvdDesc* __restrict__ descs, int NB, int ldb, double tol, int max_sweeps) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = NB / 2;
+    const int rank = static_cast<int>(cluster.block_rank());
+    const SvdDesc d = descs[blockIdx.x / CS];
+    const int n = d.n, NP = NB * kBW;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    extern __shared__ __align__(16) double sm[];
+    double* Bs = sm;                                     // 32 columns x ldb
+    double* Vs = sm + static_cast<size_t>(2 * kBW) * ldb;
+    __shared__ double s_red[32];
+    __shared__ int s_flag;
+    // global master copies and cluster-wide scratch (the problem's work buffer)
+    double* Bm = d.work;
+    double* Vm = Bm + static_cast<size_t>(n) * NP;
+    double* sig = Vm + static_cast<size_t>(n) * NP;       // NP
+    double* aux = sig + NP;                               // [0, 16): per-CTA partials; then 2 int flags
+    int* gflag = reinterpret_cast<int*>(aux + 16);
+    auto csync = [&] {
+        __threadfence();
+        if (CS > 1) cluster.sync(); else __syncthreads();
+    };
+
+    // masters: B := A (zero padding columns), V := I; ||A||_F
+    double fro = 0.0;
+    for (int64_t idx = static_cast<int64_t>(rank) * kBT + tid; idx < static_cast<int64_t>(n) * NP;
+         idx += static_cast<int64_t>(CS) * kBT) {
+        const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+        const double v = j < n ? d.A[i + static_cast<int64_t>(j) * d.lda] : 0.0;
+        Bm[idx] = v;
+        Vm[idx] = i == j ? 1.0 : 0.0;
+        fro += v * v;
+    }
+    fro = wsum(fro);
+    if (lane == 0) s_red[warp] = fro;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kBT / 32; ++w) s += s_red[w];
+        aux[rank] = s;
+        if (rank == 0) {
+            gflag[0] = 0;
+            gflag[1] = 0;
+        }
+    }
+    csync();
+    double nf2 = 0.0;
+    for (int r = 0; r < CS; ++r) nf2 += aux[r];
+    const double nf = sqrt(nf2);
+    const double eps = DBL_EPSILON;
+    const double rel = fmax(tol, sqrt(static_cast<double>(n)) * eps);
+    const double floor_col = 4.0 * static_cast<double>(n) * eps * nf;
+
+    if (n == 0 || nf == 0.0) {  // jacobi_svd.cpp:47-53: U = I, sigma = 0, V = I
+        for (int64_t idx = static_cast<int64_t>(rank) * kBT + tid; idx < static_cast<int64_t>(n) * n;
+             idx += static_cast<int64_t>(CS) * kBT) {
+            const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+            d.U[idx] = i == j ? 1.0 : 0.0;
+            d.V[idx] = i == j ? 1.0 : 0.0;
+        }
+        if (rank == 0) {
+            for (int j = tid; j < n; j += kBT) d.sigma[j] = 0.0;
+            if (tid == 0) {
+                d.status[0] = 0.0;
+                d.status[1] = 0.0;
+                d.status[2] = n;
+                d.status[3] = 0;
+            }
+        }
+        if (CS > 1) cluster.sync();
+        return;
+    }
+
+    // my two blocks <-> shared memory (block b's 16 columns -> local columns 16 h .. 16 h + 15)
+    auto load_blocks = [&](int b0, int b1) {
+        for (int idx = tid; idx < 2 * kBW * n; idx += kBT) {
+            const int col = idx / n, i = idx - col * n;
+            const int64_t g = (static_cast<int64_t>(col < kBW ? b0 : b1) * kBW + (col & (kBW - 1))) * n + i;
+            Bs[col * ldb + i] = Bm[g];
+            Vs[col * ldb + i] = Vm[g];
+        }
+        __syncthreads();
+    };
+    auto store_blocks = [&](int b0, int b1) {
+        for (int idx = tid; idx < 2 * kBW * n; idx += kBT) {
+            const int col = idx / n, i = idx - col * n;
+            const int64_t g = (static_cast<int64_t>(col < kBW ? b0 : b1) * kBW + (col & (kBW - 1))) * n + i;
+            Bm[g] = Bs[col * ldb + i];
+            Vm[g] = Vs[col * ldb + i];
+        }
+    };
+    // one sweep: every column pair once; rotate (mode 0) or only track the worst ratio (mode 1)
+    auto sweep_once = [&](int mode, double& worst) -> bool {
+        bool rot = false;
+        const int nsr = NB - 1;
+        for (int sr = 0; sr < nsr; ++sr) {
+            int b0, b1;
+            rrp(NB, sr, rank, b0, b1);
+            load_blocks(b0, b1);
+            const int nrounds = sr == 0 ? 2 * kBW - 1 : kBW;
+            for (int r = 0; r < nrounds; ++r) {
+                int lp, lq;
+                if (sr == 0) {
+                    rrp(2 * kBW, r, warp, lp, lq);
+                } else {
+                    lp = warp;
+                    lq = kBW + ((warp + r) & (kBW - 1));
+                }
+                double* bp = Bs + lp * ldb;
+                double* bq = Bs + lq * ldb;
+                double x[RPT], y[RPT];
+                double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+                for (int t = 0; t < RPT; ++t) {
+                    const int i = lane + 32 * t;
+                    x[t] = i < n ? bp[i] : 0.0;
+                    y[t] = i < n ? bq[i] : 0.0;
+                    al += x[t] * x[t];
+                    be += y[t] * y[t];
+                    ga += x[t] * y[t];
+                }
+                al = wsum(al);
+                be = wsum(be);
+                ga = wsum(ga);
+                double c = 1.0, s = 0.0, ratio = -1.0;
+                const bool go = jdecide(al, be, ga, rel, floor_col, c, s, ratio);
+                if (mode == 1 && ratio >= 0.0) worst = fmax(worst, ratio);
+                if (go && mode == 0) {
+                    rot = true;
+                    double* vp = Vs + lp * ldb;
+                    double* vq = Vs + lq * ldb;
+#pragma unroll
+                    for (int t = 0; t < RPT; ++t) {
+                        const int i = lane + 32 * t;
+                        if (i < n) {
+                            bp[i] = c * x[t] - s * y[t];
+                            bq[i] = s * x[t] + c * y[t];
+                            const double vx = vp[i], vy = vq[i];
+                            vp[i] = c * vx - s * vy;
+                            vq[i] = s * vx + c * vy;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if (mode == 0) store_blocks(b0, b1);
+            csync();
+        }
+        return rot;
+    };
+
+    bool converged = false;
+    int sweep = 0;
+    double worst = 0.0;
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+        const bool rot = sweep_once(0, worst);
+        // cluster-wide OR of "some pair rotated" through a global flag, two flags alternating
+        const int any = __syncthreads_or(rot ? 1 : 0);
+        if (tid == 0 && any) atomicOr(&gflag[sweep & 1], 1);
+        csync();
+        const int f = *reinterpret_cast<volatile int*>(&gflag[sweep & 1]);
+        if (rank == 0 && tid == 0) gflag[(sweep + 1) & 1] = 0;
+        converged = f == 0;
+        csync();
+    }
+
+    if (!converged) {  // residual: worst remaining pair ratio (jacobi_svd.cpp:97-109)
+        sweep_once(1, worst);
+        if (lane == 0) s_red[warp] = worst;
+        __syncthreads();
+        if (tid == 0) {
+            double m = 0.0;
+            for (int w = 0; w < kBT / 32; ++w) m = fmax(m, s_red[w]);
+            aux[rank] = m;
+        }
+        csync();
+        if (rank == 0 && tid == 0) {
+            double m = 0.0;
+            for (int r = 0; r < CS; ++r) m = fmax(m, aux[r]);
+            d.status[0] = RUTV_ERR_CONVERGENCE;
+            d.status[1] = m;
+            d.status[2] = n;
+            d.status[3] = sweep;
+        }
+        if (CS > 1) cluster.sync();
+        return;
+    }
+
+    // sigma_j = ||b_j||: CTA c takes blocks 2c, 2c + 1 (two columns per warp)
+    load_blocks(2 * rank, 2 * rank + 1);
+    for (int col = warp; col < 2 * kBW; col += kBT / 32) {
+        const double* b = Bs + col * ldb;
+        double a = 0.0;
+        for (int i = lane; i < n; i += 32) a += b[i] * b[i];
+        a = wsum(a);
+        if (lane == 0) sig[2 * rank * kBW + col] = sqrt(a);
+    }
+    csync();
+    // stable descending rank of each of my columns among the n real ones, then write out
+    __shared__ int s_dest[2 * kBW];
+    __shared__ double s_sig[2 * kBW];
+    if (tid < 2 * kBW) {
+        const int j = 2 * rank * kBW + tid;
+        int t = -1;
+        double sj = 0.0;
+        if (j < n) {
+            sj = sig[j];
+            t = 0;
+            for (int k = 0; k < n; ++k) {
+                const double sk = sig[k];
+                t += (sk > sj) || (k < j && sk == sj);
+            }
+        }
+        s_dest[tid] = t;
+        s_sig[tid] = sj;
+    }
+    __syncthreads();
+    for (int col = 0; col < 2 * kBW; ++col) {
+        const int t = s_dest[col];
+        if (t < 0) continue;
+        const double s = s_sig[col];
+        for (int i = tid; i < n; i += kBT) {
+            d.V[i + static_cast<int64_t>(t) * n] = Vs[col * ldb + i];
+            d.U[i + static_cast<int64_t>(t) * n] = s > floor_col ? Bs[col * ldb + i] / s : 0.0;
+        }
+        if (tid == 0) d.sigma[t] = s;
+    }
+    if (rank == 0 && tid == 0) {
+        int kept = 0;
+        for (int j = 0; j < n; ++j) kept += sig[j] > floor_col;
+        d.status[0] = 0.0;
+        d.status[1] = 0.0;
+        d.status[2] = kept;
+        d.status[3] = sweep;
+    }
+    if (CS > 1) cluster.sync();
+}
+
+int blk_nb(int n) { return n <= 32 ? 2 : n <= 64 ? 4 : n <= 128 ? 8 : 16; }
+
+template <int RPT>
+void launch_blk(cudaStream_t stream, const SvdDesc* d, int count, int NB, int ldb, size_t smem, double tol,
+                int max_sweeps) {
+    auto k = jacobi_blk_kernel<RPT>;
+    once_per_device(reinterpret_cast<const void*>(k), [k] {
+        RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       dyn_smem_cap(reinterpret_cast<const void*>(k))));
+    });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(count * (NB / 2)));
+    cfg.blockDim = dim3(kBT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = static_cast<unsigned>(NB / 2);
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    RUTV_CUDA(cudaLaunchKernelEx(&cfg, k, d, NB, ldb, tol, max_sweeps));
+}
+
+}  // namespace
+
+// Work doubles the column-distributed kernel needs for an n x n problem inside a batch whose
+// largest block is <= 256 wide: two n x 256 master copies, sigma, scratch (jacobi.cu adds its own).
+int64_t svd_blk_work_elems(int64_t n) { return n <= 256 ? 2 * n * 256 + 256 + 64 : 0; }
+
+// nmax <= 256 and not disabled (RUTV_JACOBI=rows selects the row-distributed kernel of jacobi.cu)
+bool svd_blk_applicable(int nmax) {
+    static const bool off = [] {
+        const char* e = std::getenv("RUTV_JACOBI");
+        return e && std::strcmp(e, "rows") == 0;
+    }();
+    return !off && nmax >= 1 && nmax <= 256;
+}
+
+void svd_batch_blk(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol, int max_sweeps) {
+    const int NB = blk_nb(nmax);
+    const int rpt = (nmax + 31) / 32;
+    const int RPT = rpt <= 1 ? 1 : rpt <= 2 ? 2 : rpt <= 4 ? 4 : 8;
+    const int ldb = 32 * RPT + 1;
+    const size_t smem = static_cast<size_t>(2) * (2 * kBW) * ldb * sizeof(double);
+    switch (RPT) {
+        case 1: launch_blk<1>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        case 2: launch_blk<2>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        case 4: launch_blk<4>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        default: launch_blk<8>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+    }
+    note_launch();
+    RUTV_CHECK_LAUNCH();
+}
+
+}  // namespace rutv
