@@ -8,8 +8,11 @@
 // so every pair's three dot products cross the cluster every round (one DSMEM exchange + two CTA
 // barriers per round, ~5 K cycles for n = 128).  Here the block's columns are cut into NB = 2 CS
 // column blocks of 16; a CTA holds TWO column blocks (32 whole columns of B and of V) in shared
-// memory and one WARP owns a pair: dots, decision and rotation are warp-local (shuffles only), a
-// round costs one CTA barrier, and the cluster only meets when the column blocks are re-paired:
+// memory and one HALF-WARP owns a pair: dots, decision and rotation are warp-local (shuffles
+// only; the two pairs of a warp share every instruction -- with a full warp per pair the round was
+// bound by the SM's shuffle and FP64 issue rates, 2.5 K cycles, all 32 lanes repeating one pair's
+// square roots and divisions), a round costs one CTA barrier, and the cluster only meets when the
+// column blocks are re-paired:
 //   super-round sr of a sweep: CTA c takes the block pair rr_pair(NB, sr, c) of a round-robin
 //   tournament over the blocks; the first super-round rotates all 31 x 16 pairs of its 32
 //   columns, the others only the 16 x 16 cross pairs -- 31 + (NB - 2) 16 = N - 1 rounds per
@@ -20,6 +23,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -31,12 +35,18 @@ namespace rutv {
 
 namespace {
 
-constexpr int kBT = 512;  // threads: 16 warps = the 16 pairs of a local round
+constexpr int kBT = 256;  // threads: 8 warps x 2 half-warps = the 16 pairs of a local round
 constexpr int kBW = 16;   // columns per block
+constexpr int kHL = 16;   // lanes per pair
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double hsum(double v) {  // over the 16 lanes of a half-warp
+#pragma unroll
+    for (int o = kHL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
@@ -53,23 +63,23 @@ __device__ __forceinline__ void rrp(int N, int r, int pi, int& p, int& q) {
     q = max(x, y);
 }
 
-// jacobi_svd.cpp:60-85: skip tests and the rotation (c, s) of a pair from its three dots
-__device__ __forceinline__ bool jdecide(double al, double be, double ga, double rel, double floor_col, double& c,
-                                        double& s, double& ratio) {
-    const double np = sqrt(al), nq = sqrt(be);
+// jacobi_svd.cpp:60-85: skip tests and the rotation (c, s) of a pair from its three dots.  The
+// skip tests in squared form (no square roots: ||b|| <= floor <=> ||b||^2 <= floor^2,
+// |g| <= rel ||p|| ||q|| <=> g^2 <= rel^2 a b) come first, so a pair that does not rotate costs
+// a few multiplies; the rotation itself is the reference's formula.
+__device__ __forceinline__ bool jskip(double al, double be, double ga, double rel2, double floor2) {
+    return al <= floor2 || be <= floor2 || ga * ga <= rel2 * (al * be);
+}
+__device__ __forceinline__ void jrot(double al, double be, double ga, double& c, double& s) {
     const double zeta = (be - al) / (2.0 * ga);
-    ratio = -1.0;
-    if (np <= floor_col || nq <= floor_col) return false;
-    const double pq = np * nq;
-    ratio = fabs(ga) / pq;
-    if (fabs(ga) <= rel * pq) return false;
     const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
     c = rsqrt(1.0 + tt * tt);
     s = c * tt;
-    return true;
 }
 
-template <int RPT>  // rows per lane: n <= 32 RPT
+__device__ long long* g_jbtrace = nullptr;  // debug: RUTV_JAC_TRACE per-round clock64 of CTA 0, warp 0
+
+template <int RPT>  // rows per lane of a pair: n <= 16 RPT
 __global__ void __launch_bounds__(kBT, 1)
     jacobi_blk_kernel(const SvdDesc* __restrict__ descs, int NB, int ldb, double tol, int max_sweeps) {
     cg::cluster_group cluster = cg::this_cluster();
@@ -123,6 +133,8 @@ __global__ void __launch_bounds__(kBT, 1)
     const double eps = DBL_EPSILON;
     const double rel = fmax(tol, sqrt(static_cast<double>(n)) * eps);
     const double floor_col = 4.0 * static_cast<double>(n) * eps * nf;
+    const double rel2 = rel * rel, floor2 = floor_col * floor_col;
+    const int hl = lane & (kHL - 1), ph = lane >> 4;  // lane within the pair, which pair of the warp
 
     if (n == 0 || nf == 0.0) {  // jacobi_svd.cpp:47-53: U = I, sigma = 0, V = I
         for (int64_t idx = static_cast<int64_t>(rank) * kBT + tid; idx < static_cast<int64_t>(n) * n;
@@ -144,24 +156,52 @@ __global__ void __launch_bounds__(kBT, 1)
         return;
     }
 
-    // my two blocks <-> shared memory (block b's 16 columns -> local columns 16 h .. 16 h + 15)
+    // my two blocks <-> shared memory (block b's 16 columns -> local columns 16 h .. 16 h + 15):
+    // warp w moves local columns w and w + 16, lanes along the rows (coalesced), every load of the
+    // warp's 4 RPT in flight before the first store
+    constexpr int RL = (RPT + 1) / 2;  // rows per lane when all 32 lanes run along a column
     auto load_blocks = [&](int b0, int b1) {
-        for (int idx = tid; idx < 2 * kBW * n; idx += kBT) {
-            const int col = idx / n, i = idx - col * n;
-            const int64_t g = (static_cast<int64_t>(col < kBW ? b0 : b1) * kBW + (col & (kBW - 1))) * n + i;
-            Bs[col * ldb + i] = Bm[g];
-            Vs[col * ldb + i] = Vm[g];
+        double vb[4][RL], vv[4][RL];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int col = warp + 8 * h;  // local column; block b0 holds 0..15, b1 16..31
+            const int64_t g = (static_cast<int64_t>(col < kBW ? b0 : b1) * kBW + (col & (kBW - 1))) * n;
+#pragma unroll
+            for (int t = 0; t < RL; ++t) {
+                const int i = lane + 32 * t;
+                vb[h][t] = i < n ? __ldcg(Bm + g + i) : 0.0;
+                vv[h][t] = i < n ? __ldcg(Vm + g + i) : 0.0;
+            }
         }
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+            for (int t = 0; t < RL; ++t) {
+                const int i = lane + 32 * t;
+                if (i < n) {
+                    Bs[(warp + 8 * h) * ldb + i] = vb[h][t];
+                    Vs[(warp + 8 * h) * ldb + i] = vv[h][t];
+                }
+            }
         __syncthreads();
     };
     auto store_blocks = [&](int b0, int b1) {
-        for (int idx = tid; idx < 2 * kBW * n; idx += kBT) {
-            const int col = idx / n, i = idx - col * n;
-            const int64_t g = (static_cast<int64_t>(col < kBW ? b0 : b1) * kBW + (col & (kBW - 1))) * n + i;
-            Bm[g] = Bs[col * ldb + i];
-            Vm[g] = Vs[col * ldb + i];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int col = warp + 8 * h;
+            const int64_t g = (static_cast<int64_t>(col < kBW ? b0 : b1) * kBW + (col & (kBW - 1))) * n;
+#pragma unroll
+            for (int t = 0; t < RL; ++t) {
+                const int i = lane + 32 * t;
+                if (i < n) {
+                    __stcg(Bm + g + i, Bs[col * ldb + i]);
+                    __stcg(Vm + g + i, Vs[col * ldb + i]);
+                }
+            }
         }
     };
+    long long* const jtr = (g_jbtrace && blockIdx.x == 0 && tid == 0) ? g_jbtrace : nullptr;
+    int gr = 0;  // rounds done (trace index)
     // one sweep: every column pair once; rotate (mode 0) or only track the worst ratio (mode 1)
     auto sweep_once = [&](int mode, double& worst) -> bool {
         bool rot = false;
@@ -172,52 +212,64 @@ __global__ void __launch_bounds__(kBT, 1)
             load_blocks(b0, b1);
             const int nrounds = sr == 0 ? 2 * kBW - 1 : kBW;
             for (int r = 0; r < nrounds; ++r) {
+                const int pi = 2 * warp + ph;  // this half-warp's pair of the round
                 int lp, lq;
                 if (sr == 0) {
-                    rrp(2 * kBW, r, warp, lp, lq);
+                    rrp(2 * kBW, r, pi, lp, lq);
                 } else {
-                    lp = warp;
-                    lq = kBW + ((warp + r) & (kBW - 1));
+                    lp = pi;
+                    lq = kBW + ((pi + r) & (kBW - 1));
                 }
+                if (jtr && gr < 48) jtr[gr * 6 + 0] = clock64();
                 double* bp = Bs + lp * ldb;
                 double* bq = Bs + lq * ldb;
                 double x[RPT], y[RPT];
                 double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
                 for (int t = 0; t < RPT; ++t) {
-                    const int i = lane + 32 * t;
+                    const int i = hl + kHL * t;
                     x[t] = i < n ? bp[i] : 0.0;
                     y[t] = i < n ? bq[i] : 0.0;
                     al += x[t] * x[t];
                     be += y[t] * y[t];
                     ga += x[t] * y[t];
                 }
-                al = wsum(al);
-                be = wsum(be);
-                ga = wsum(ga);
-                double c = 1.0, s = 0.0, ratio = -1.0;
-                const bool go = jdecide(al, be, ga, rel, floor_col, c, s, ratio);
-                if (mode == 1 && ratio >= 0.0) worst = fmax(worst, ratio);
-                if (go && mode == 0) {
-                    rot = true;
-                    double* vp = Vs + lp * ldb;
-                    double* vq = Vs + lq * ldb;
+                al = hsum(al);
+                be = hsum(be);
+                ga = hsum(ga);
+                if (jtr && gr < 48) jtr[gr * 6 + 1] = clock64();
+                const bool skip = jskip(al, be, ga, rel2, floor2);
+                if (mode == 1) {
+                    if (!(al <= floor2 || be <= floor2)) worst = fmax(worst, fabs(ga) / sqrt(al * be));
+                } else if (__any_sync(0xffffffffu, !skip)) {
+                    double c = 1.0, s = 0.0;
+                    jrot(al, be, ga, c, s);
+                    if (jtr && gr < 48) jtr[gr * 6 + 2] = clock64();
+                    if (!skip) {
+                        rot = true;
+                        double* vp = Vs + lp * ldb;
+                        double* vq = Vs + lq * ldb;
 #pragma unroll
-                    for (int t = 0; t < RPT; ++t) {
-                        const int i = lane + 32 * t;
-                        if (i < n) {
-                            bp[i] = c * x[t] - s * y[t];
-                            bq[i] = s * x[t] + c * y[t];
-                            const double vx = vp[i], vy = vq[i];
-                            vp[i] = c * vx - s * vy;
-                            vq[i] = s * vx + c * vy;
+                        for (int t = 0; t < RPT; ++t) {
+                            const int i = hl + kHL * t;
+                            if (i < n) {
+                                bp[i] = c * x[t] - s * y[t];
+                                bq[i] = s * x[t] + c * y[t];
+                                const double vx = vp[i], vy = vq[i];
+                                vp[i] = c * vx - s * vy;
+                                vq[i] = s * vx + c * vy;
+                            }
                         }
                     }
                 }
+                if (jtr && gr < 48) jtr[gr * 6 + 3] = clock64();
                 __syncthreads();
+                if (jtr && gr < 48) jtr[gr * 6 + 4] = clock64();
+                ++gr;
             }
             if (mode == 0) store_blocks(b0, b1);
             csync();
+            if (jtr && gr < 48) jtr[gr * 6 + 5] = clock64();
         }
         return rot;
     };
@@ -239,6 +291,7 @@ __global__ void __launch_bounds__(kBT, 1)
 
     if (!converged) {  // residual: worst remaining pair ratio (jacobi_svd.cpp:97-109)
         sweep_once(1, worst);
+        worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, 16));
         if (lane == 0) s_red[warp] = worst;
         __syncthreads();
         if (tid == 0) {
@@ -259,7 +312,7 @@ __global__ void __launch_bounds__(kBT, 1)
         return;
     }
 
-    // sigma_j = ||b_j||: CTA c takes blocks 2c, 2c + 1 (two columns per warp)
+    // sigma_j = ||b_j||: CTA c takes blocks 2c, 2c + 1 (four columns per warp)
     load_blocks(2 * rank, 2 * rank + 1);
     for (int col = warp; col < 2 * kBW; col += kBT / 32) {
         const double* b = Bs + col * ldb;
@@ -331,7 +384,26 @@ void launch_blk(cudaStream_t stream, const SvdDesc* d, int count, int NB, int ld
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
+    static const bool jtrace = std::getenv("RUTV_JAC_TRACE") != nullptr;
+    long long* dtr = nullptr;
+    if (jtrace) {
+        RUTV_CUDA(cudaMalloc(&dtr, 49 * 6 * sizeof(long long)));
+        RUTV_CUDA(cudaMemset(dtr, 0, 49 * 6 * sizeof(long long)));
+        RUTV_CUDA(cudaMemcpyToSymbol(g_jbtrace, &dtr, sizeof(dtr)));
+    }
     RUTV_CUDA(cudaLaunchKernelEx(&cfg, k, d, NB, ldb, tol, max_sweeps));
+    if (jtrace) {
+        long long h[49 * 6];
+        RUTV_CUDA(cudaStreamSynchronize(stream));
+        RUTV_CUDA(cudaMemcpy(h, dtr, sizeof(h), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "jacobi_blk trace NB=%d (cycles: dots, decide, rotate, barrier; exchange after the super-round)\n", NB);
+        for (int r = 0; r < 48; ++r)
+            std::fprintf(stderr, "  round %2d: %6lld %6lld %6lld %6lld   %6lld\n", r, h[r * 6 + 1] - h[r * 6], h[r * 6 + 2] - h[r * 6 + 1],
+                         h[r * 6 + 3] - h[r * 6 + 2], h[r * 6 + 4] - h[r * 6 + 3], h[r * 6 + 5] ? h[r * 6 + 5] - h[(r - 1) * 6 + 4] : 0LL);
+        long long* z = nullptr;
+        RUTV_CUDA(cudaMemcpyToSymbol(g_jbtrace, &z, sizeof(z)));
+        cudaFree(dtr);
+    }
 }
 
 }  // namespace
@@ -351,15 +423,15 @@ bool svd_blk_applicable(int nmax) {
 
 void svd_batch_blk(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol, int max_sweeps) {
     const int NB = blk_nb(nmax);
-    const int rpt = (nmax + 31) / 32;
-    const int RPT = rpt <= 1 ? 1 : rpt <= 2 ? 2 : rpt <= 4 ? 4 : 8;
-    const int ldb = 32 * RPT + 1;
+    const int rpt = (nmax + kHL - 1) / kHL;
+    const int RPT = rpt <= 2 ? 2 : rpt <= 4 ? 4 : rpt <= 8 ? 8 : 16;
+    const int ldb = kHL * RPT + 1;
     const size_t smem = static_cast<size_t>(2) * (2 * kBW) * ldb * sizeof(double);
     switch (RPT) {
-        case 1: launch_blk<1>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
         case 2: launch_blk<2>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
         case 4: launch_blk<4>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
-        default: launch_blk<8>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        case 8: launch_blk<8>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        default: launch_blk<16>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
     }
     note_launch();
     RUTV_CHECK_LAUNCH();
