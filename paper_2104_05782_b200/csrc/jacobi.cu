@@ -616,7 +616,7 @@ int64_t svd_work_elems(int64_t n, int /*max_sweeps*/) {
 void svd_batch(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol,
                int max_sweeps) {
     if (count <= 0) return;
-    if (svd_blk_applicable(nmax)) {  // blocks up to 256 wide: the column-distributed kernel (jacobi_blk.cu)
+    if (svd_blk_applicable(nmax)) {  // blocks up to 512 wide: the column-distributed kernel (jacobi_blk.cu)
         svd_batch_blk(stream, d_descs, count, nmax, tol, max_sweeps);
         complete_kernel<<<count, 256, 0, stream>>>(d_descs);
         note_launch();

@@ -1,4 +1,4 @@
-// jacobi_blk.cu -- batched one-sided Jacobi SVD with COLUMN-distributed blocks (n <= 256).
+// jacobi_blk.cu -- batched one-sided Jacobi SVD with COLUMN-distributed blocks (n <= 512).
 //
 // Same algorithm contract as jacobi.cu (reference proj/src/jacobi_svd.cpp:39-148: one-sided
 // Jacobi on the columns of a square block, thresholds rel = max(tol, sqrt(n) eps) and
@@ -18,7 +18,11 @@
 //   columns, the others only the 16 x 16 cross pairs -- 31 + (NB - 2) 16 = N - 1 rounds per
 //   sweep, every column pair exactly once.
 // Between super-rounds the blocks live in a global master copy (the problem's work buffer, L2
-// resident): store both blocks, fence, cluster barrier, load the next two.
+// resident): store both blocks, fence, cluster barrier, load the next two.  V never enters shared
+// memory: the rotations of a super-round are accumulated in a 32 x 32 matrix J (two rows per lane
+// instead of n / 16), and V(:, my 32 columns) <- V(:, my 32 columns) J is applied to the master copy
+// once per super-round -- half the shared-memory traffic of a round (which bounds it), and blocks
+// up to 512 wide fit (32 columns of B: 131 KB).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -89,8 +93,9 @@ __global__ void __launch_bounds__(kBT, 1)
     const int n = d.n, NP = NB * kBW;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     extern __shared__ __align__(16) double sm[];
-    double* Bs = sm;                                     // 32 columns x ldb
-    double* Vs = sm + static_cast<size_t>(2 * kBW) * ldb;
+    constexpr int LJ = 2 * kBW + 1;
+    double* Bs = sm;                                           // 32 columns x ldb
+    double* Js = sm + static_cast<size_t>(2 * kBW) * ldb;      // J (32 x 32, column c at Js + c LJ)
     __shared__ double s_red[32];
     __shared__ int s_flag;
     // global master copies and cluster-wide scratch (the problem's work buffer)
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(kBT, 1)
     // warp's 4 RPT in flight before the first store
     constexpr int RL = (RPT + 1) / 2;  // rows per lane when all 32 lanes run along a column
     auto load_blocks = [&](int b0, int b1) {
-        double vb[4][RL], vv[4][RL];
+        double vb[4][RL];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int col = warp + 8 * h;  // local column; block b0 holds 0..15, b1 16..31
@@ -170,7 +175,6 @@ __global__ void __launch_bounds__(kBT, 1)
             for (int t = 0; t < RL; ++t) {
                 const int i = lane + 32 * t;
                 vb[h][t] = i < n ? __ldcg(Bm + g + i) : 0.0;
-                vv[h][t] = i < n ? __ldcg(Vm + g + i) : 0.0;
             }
         }
 #pragma unroll
@@ -178,14 +182,14 @@ __global__ void __launch_bounds__(kBT, 1)
 #pragma unroll
             for (int t = 0; t < RL; ++t) {
                 const int i = lane + 32 * t;
-                if (i < n) {
-                    Bs[(warp + 8 * h) * ldb + i] = vb[h][t];
-                    Vs[(warp + 8 * h) * ldb + i] = vv[h][t];
-                }
+                if (i < n) Bs[(warp + 8 * h) * ldb + i] = vb[h][t];
             }
+        for (int e = tid; e < 2 * kBW * 2 * kBW; e += kBT) Js[(e >> 5) * LJ + (e & 31)] = (e >> 5) == (e & 31) ? 1.0 : 0.0;
         __syncthreads();
     };
-    auto store_blocks = [&](int b0, int b1) {
+    // B blocks back to the master; V(:, my 32 columns) <- V(:, my 32 columns) J on the master (a row
+    // of V per thread: 32 coalesced loads, 32 x 32 fmas against J from shared memory, 32 stores)
+    auto store_blocks = [&](int b0, int b1, bool rotated) {
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int col = warp + 8 * h;
@@ -193,10 +197,25 @@ __global__ void __launch_bounds__(kBT, 1)
 #pragma unroll
             for (int t = 0; t < RL; ++t) {
                 const int i = lane + 32 * t;
-                if (i < n) {
-                    __stcg(Bm + g + i, Bs[col * ldb + i]);
-                    __stcg(Vm + g + i, Vs[col * ldb + i]);
+                if (i < n) __stcg(Bm + g + i, Bs[col * ldb + i]);
+            }
+        }
+        if (!rotated) return;  // J = I
+        for (int i = tid; i < n; i += kBT) {
+            double v[2 * kBW];
+#pragma unroll
+            for (int k = 0; k < 2 * kBW; ++k)
+                v[k] = __ldcg(Vm + (static_cast<int64_t>(k < kBW ? b0 : b1) * kBW + (k & (kBW - 1))) * n + i);
+#pragma unroll 2
+            for (int c = 0; c < 2 * kBW; ++c) {
+                const double* jc = Js + c * LJ;
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < 2 * kBW; k += 2) {
+                    a0 = __fma_rn(v[k], jc[k], a0);
+                    a1 = __fma_rn(v[k + 1], jc[k + 1], a1);
                 }
+                __stcg(Vm + (static_cast<int64_t>(c < kBW ? b0 : b1) * kBW + (c & (kBW - 1))) * n + i, a0 + a1);
             }
         }
     };
@@ -210,6 +229,7 @@ __global__ void __launch_bounds__(kBT, 1)
             int b0, b1;
             rrp(NB, sr, rank, b0, b1);
             load_blocks(b0, b1);
+            bool rot_sr = false;  // some pair of this super-round rotated (J != I)
             const int nrounds = sr == 0 ? 2 * kBW - 1 : kBW;
             for (int r = 0; r < nrounds; ++r) {
                 const int pi = 2 * warp + ph;  // this half-warp's pair of the round
@@ -247,18 +267,23 @@ __global__ void __launch_bounds__(kBT, 1)
                     if (jtr && gr < 48) jtr[gr * 6 + 2] = clock64();
                     if (!skip) {
                         rot = true;
-                        double* vp = Vs + lp * ldb;
-                        double* vq = Vs + lq * ldb;
+                        rot_sr = true;
 #pragma unroll
                         for (int t = 0; t < RPT; ++t) {
                             const int i = hl + kHL * t;
                             if (i < n) {
                                 bp[i] = c * x[t] - s * y[t];
                                 bq[i] = s * x[t] + c * y[t];
-                                const double vx = vp[i], vy = vq[i];
-                                vp[i] = c * vx - s * vy;
-                                vq[i] = s * vx + c * vy;
                             }
+                        }
+                        double* jp = Js + lp * LJ;
+                        double* jq = Js + lq * LJ;
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            const int i = hl + kHL * t;
+                            const double vx = jp[i], vy = jq[i];
+                            jp[i] = c * vx - s * vy;
+                            jq[i] = s * vx + c * vy;
                         }
                     }
                 }
@@ -267,7 +292,10 @@ __global__ void __launch_bounds__(kBT, 1)
                 if (jtr && gr < 48) jtr[gr * 6 + 4] = clock64();
                 ++gr;
             }
-            if (mode == 0) store_blocks(b0, b1);
+            if (mode == 0) {
+                const bool srot = __syncthreads_or(rot_sr ? 1 : 0) != 0;
+                store_blocks(b0, b1, srot);
+            }
             csync();
             if (jtr && gr < 48) jtr[gr * 6 + 5] = clock64();
         }
@@ -346,7 +374,7 @@ __global__ void __launch_bounds__(kBT, 1)
         if (t < 0) continue;
         const double s = s_sig[col];
         for (int i = tid; i < n; i += kBT) {
-            d.V[i + static_cast<int64_t>(t) * n] = Vs[col * ldb + i];
+            d.V[i + static_cast<int64_t>(t) * n] = __ldcg(Vm + (static_cast<int64_t>(2 * rank) * kBW + col) * n + i);
             d.U[i + static_cast<int64_t>(t) * n] = s > floor_col ? Bs[col * ldb + i] / s : 0.0;
         }
         if (tid == 0) d.sigma[t] = s;
@@ -362,13 +390,14 @@ __global__ void __launch_bounds__(kBT, 1)
     if (CS > 1) cluster.sync();
 }
 
-int blk_nb(int n) { return n <= 32 ? 2 : n <= 64 ? 4 : n <= 128 ? 8 : 16; }
+int blk_nb(int n) { return n <= 32 ? 2 : n <= 64 ? 4 : n <= 128 ? 8 : n <= 256 ? 16 : 32; }
 
 template <int RPT>
 void launch_blk(cudaStream_t stream, const SvdDesc* d, int count, int NB, int ldb, size_t smem, double tol,
                 int max_sweeps) {
     auto k = jacobi_blk_kernel<RPT>;
     once_per_device(reinterpret_cast<const void*>(k), [k] {
+        RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));  // 16 CTAs at n = 512
         RUTV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        dyn_smem_cap(reinterpret_cast<const void*>(k))));
     });
@@ -409,29 +438,30 @@ void launch_blk(cudaStream_t stream, const SvdDesc* d, int count, int NB, int ld
 }  // namespace
 
 // Work doubles the column-distributed kernel needs for an n x n problem inside a batch whose
-// largest block is <= 256 wide: two n x 256 master copies, sigma, scratch (jacobi.cu adds its own).
-int64_t svd_blk_work_elems(int64_t n) { return n <= 256 ? 2 * n * 256 + 256 + 64 : 0; }
+// largest block is <= 512 wide: two n x 512 master copies, sigma, scratch (jacobi.cu adds its own).
+int64_t svd_blk_work_elems(int64_t n) { return n <= 512 ? 2 * n * 512 + 512 + 64 : 0; }
 
-// nmax <= 256 and not disabled (RUTV_JACOBI=rows selects the row-distributed kernel of jacobi.cu)
+// nmax <= 512 and not disabled (RUTV_JACOBI=rows selects the row-distributed kernel of jacobi.cu)
 bool svd_blk_applicable(int nmax) {
     static const bool off = [] {
         const char* e = std::getenv("RUTV_JACOBI");
         return e && std::strcmp(e, "rows") == 0;
     }();
-    return !off && nmax >= 1 && nmax <= 256;
+    return !off && nmax >= 1 && nmax <= 512;
 }
 
 void svd_batch_blk(cudaStream_t stream, const SvdDesc* d_descs, int count, int nmax, double tol, int max_sweeps) {
     const int NB = blk_nb(nmax);
     const int rpt = (nmax + kHL - 1) / kHL;
-    const int RPT = rpt <= 2 ? 2 : rpt <= 4 ? 4 : rpt <= 8 ? 8 : 16;
+    const int RPT = rpt <= 2 ? 2 : rpt <= 4 ? 4 : rpt <= 8 ? 8 : rpt <= 16 ? 16 : 32;
     const int ldb = kHL * RPT + 1;
-    const size_t smem = static_cast<size_t>(2) * (2 * kBW) * ldb * sizeof(double);
+    const size_t smem = (static_cast<size_t>(2 * kBW) * ldb + static_cast<size_t>(2 * kBW) * (2 * kBW + 1)) * sizeof(double);
     switch (RPT) {
         case 2: launch_blk<2>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
         case 4: launch_blk<4>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
         case 8: launch_blk<8>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
-        default: launch_blk<16>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        case 16: launch_blk<16>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
+        default: launch_blk<32>(stream, d_descs, count, NB, ldb, smem, tol, max_sweeps); break;
     }
     note_launch();
     RUTV_CHECK_LAUNCH();
