@@ -97,7 +97,6 @@ __global__ void __launch_bounds__(kBT, 1)
     double* Bs = sm;                                           // 32 columns x ldb
     double* Js = sm + static_cast<size_t>(2 * kBW) * ldb;      // J (32 x 32, column c at Js + c LJ)
     __shared__ double s_red[32];
-    __shared__ int s_flag;
     // global master copies and cluster-wide scratch (the problem's work buffer)
     double* Bm = d.work;
     double* Vm = Bm + static_cast<size_t>(n) * NP;
@@ -133,7 +132,7 @@ __global__ void __launch_bounds__(kBT, 1)
     }
     csync();
     double nf2 = 0.0;
-    for (int r = 0; r < CS; ++r) nf2 += aux[r];
+    for (int r = 0; r < CS; ++r) nf2 += __ldcg(aux + r);  // other CTAs' stores: read at L2
     const double nf = sqrt(nf2);
     const double eps = DBL_EPSILON;
     const double rel = fmax(tol, sqrt(static_cast<double>(n)) * eps);
@@ -330,7 +329,7 @@ __global__ void __launch_bounds__(kBT, 1)
         csync();
         if (rank == 0 && tid == 0) {
             double m = 0.0;
-            for (int r = 0; r < CS; ++r) m = fmax(m, aux[r]);
+            for (int r = 0; r < CS; ++r) m = fmax(m, __ldcg(aux + r));
             d.status[0] = RUTV_ERR_CONVERGENCE;
             d.status[1] = m;
             d.status[2] = n;
@@ -358,10 +357,10 @@ __global__ void __launch_bounds__(kBT, 1)
         int t = -1;
         double sj = 0.0;
         if (j < n) {
-            sj = sig[j];
+            sj = __ldcg(sig + j);
             t = 0;
             for (int k = 0; k < n; ++k) {
-                const double sk = sig[k];
+                const double sk = __ldcg(sig + k);
                 t += (sk > sj) || (k < j && sk == sj);
             }
         }
@@ -381,7 +380,7 @@ __global__ void __launch_bounds__(kBT, 1)
     }
     if (rank == 0 && tid == 0) {
         int kept = 0;
-        for (int j = 0; j < n; ++j) kept += sig[j] > floor_col;
+        for (int j = 0; j < n; ++j) kept += __ldcg(sig + j) > floor_col;
         d.status[0] = 0.0;
         d.status[1] = 0.0;
         d.status[2] = kept;

@@ -14,7 +14,7 @@ def launches(path, out):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr, data = rows[0], rows[1:]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    marks = [i for i, r in enumerate(data) if "jacobi_kernel" in r[ki]]
+    marks = [i for i, r in enumerate(data) if "jacobi_kernel" in r[ki] or "jacobi_blk_kernel" in r[ki]]
     seg = data[marks[0] + 1: marks[1] + 1] if len(marks) >= 2 else data
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for r in seg:
