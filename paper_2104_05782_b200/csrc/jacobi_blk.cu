@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "cluster_msg.cuh"
 #include "rutv_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -96,6 +97,11 @@ __global__ void __launch_bounds__(kBT, 1)
     constexpr int LJ = 2 * kBW + 1;
     double* Bs = sm;                                           // 32 columns x ldb
     double* Js = sm + static_cast<size_t>(2 * kBW) * ldb;      // J (32 x 32, column c at Js + c LJ)
+    // the round body addresses shared memory from one opaque register (no special-register reads
+    // rematerialised per round, see qr_reg.cu)
+    uint32_t bs_a;
+    asm volatile("mov.u32 %0, %1;" : "=r"(bs_a) : "r"(smem_u32(sm)));
+    const uint32_t js_a = bs_a + 8u * static_cast<uint32_t>(2 * kBW * ldb);
     __shared__ double s_red[32];
     // global master copies and cluster-wide scratch (the problem's work buffer)
     double* Bm = d.work;
@@ -240,15 +246,15 @@ __global__ void __launch_bounds__(kBT, 1)
                     lq = kBW + ((pi + r) & (kBW - 1));
                 }
                 if (jtr && gr < 48) jtr[gr * 6 + 0] = clock64();
-                double* bp = Bs + lp * ldb;
-                double* bq = Bs + lq * ldb;
+                const uint32_t bp = bs_a + 8u * static_cast<uint32_t>(lp * ldb + hl);
+                const uint32_t bq = bs_a + 8u * static_cast<uint32_t>(lq * ldb + hl);
                 double x[RPT], y[RPT];
                 double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
                 for (int t = 0; t < RPT; ++t) {
-                    const int i = hl + kHL * t;
-                    x[t] = i < n ? bp[i] : 0.0;
-                    y[t] = i < n ? bq[i] : 0.0;
+                    const bool in = hl + kHL * t < n;
+                    x[t] = in ? lds_f64(bp + 8u * (kHL * t)) : 0.0;
+                    y[t] = in ? lds_f64(bq + 8u * (kHL * t)) : 0.0;
                     al += x[t] * x[t];
                     be += y[t] * y[t];
                     ga += x[t] * y[t];
@@ -269,20 +275,18 @@ __global__ void __launch_bounds__(kBT, 1)
                         rot_sr = true;
 #pragma unroll
                         for (int t = 0; t < RPT; ++t) {
-                            const int i = hl + kHL * t;
-                            if (i < n) {
-                                bp[i] = c * x[t] - s * y[t];
-                                bq[i] = s * x[t] + c * y[t];
+                            if (hl + kHL * t < n) {
+                                sts_f64(bp + 8u * (kHL * t), c * x[t] - s * y[t]);
+                                sts_f64(bq + 8u * (kHL * t), s * x[t] + c * y[t]);
                             }
                         }
-                        double* jp = Js + lp * LJ;
-                        double* jq = Js + lq * LJ;
+                        const uint32_t jp = js_a + 8u * static_cast<uint32_t>(lp * LJ + hl);
+                        const uint32_t jq = js_a + 8u * static_cast<uint32_t>(lq * LJ + hl);
 #pragma unroll
                         for (int t = 0; t < 2; ++t) {
-                            const int i = hl + kHL * t;
-                            const double vx = jp[i], vy = jq[i];
-                            jp[i] = c * vx - s * vy;
-                            jq[i] = s * vx + c * vy;
+                            const double vx = lds_f64(jp + 8u * (kHL * t)), vy = lds_f64(jq + 8u * (kHL * t));
+                            sts_f64(jp + 8u * (kHL * t), c * vx - s * vy);
+                            sts_f64(jq + 8u * (kHL * t), s * vx + c * vy);
                         }
                     }
                 }
